@@ -1,0 +1,137 @@
+/*
+ * walkjoin_b200.h -- C ABI of the B200 walk -> RPE -> join hot path.
+ *
+ * Every entry point takes DEVICE pointers owned by the caller, plain sizes
+ * and a cudaStream_t (passed as void*), launches asynchronously on that
+ * stream and returns WJ_OK or an error code; wj_last_error() gives the
+ * message of the last failure on the calling host thread.  Nothing is
+ * allocated inside and there is no global mutable state, so the library is
+ * safe to drive from several host threads on different streams.
+ *
+ * Each function names the reference interface it replaces
+ * (/root/reference/pkg/src/walkjoin/<file>:<line>).  The reference binds its
+ * numba kernels from Python; INTEGRATION.md shows the ctypes stub a
+ * maintainer adds to call these instead.
+ */
+#ifndef WALKJOIN_B200_H
+#define WALKJOIN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WJ_ABI_VERSION 1
+
+#define WJ_OK 0
+#define WJ_ERR_ARG 1          /* bad argument (maps to ValueError) */
+#define WJ_ERR_CUDA 2         /* CUDA launch/runtime failure */
+#define WJ_ERR_UNSUPPORTED 3  /* shape outside the kernels' envelope */
+
+/* dense element types for wj_join / wj_gather_rpe */
+#define WJ_F32 0
+#define WJ_F64 1
+#define WJ_BF16 2
+#define WJ_F16 3
+
+typedef void *wj_stream_t; /* cudaStream_t */
+
+int wj_abi_version(void);
+const char *wj_last_error(void);
+
+/* Walk sampling for anchors [lo, hi): walks_out[(u-lo), M, L+1] int32.
+ * Replaces _kernels.sample_all_walks (_kernels.py:69-74) as driven by
+ * sampler.preprocess (sampler.py:114-115).  Bit-exact with the reference
+ * splitmix64 stream: walk j step i of u draws mix64(S0(u) + (j*L+i)*G).
+ * idxptr is int32 (idxptr_bytes=4, requires 2E < 2^31) or int64 (8).
+ * fix_flags: [hi-lo] uint8 scratch, zeroed by the caller; anchors whose
+ * walks hit a mid-walk dead end (only possible in a non-symmetric CSR) are
+ * flagged and re-sampled sequentially on device by a second launch. */
+int wj_sample_walks(const void *idxptr, int idxptr_bytes, const int32_t *indices, int64_t n_nodes,
+                    int64_t lo, int64_t hi, int32_t num_walks, int32_t num_steps, uint64_t seed,
+                    int32_t *walks_out, uint8_t *fix_flags, wj_stream_t stream);
+
+/* One anchor from an explicit stream state; writes the end state.
+ * Replaces _kernels.sample_node_walks (_kernels.py:53-66) as used by
+ * sampler.sample_walks (sampler.py:61-76). */
+int wj_sample_node_walks(const void *idxptr, int idxptr_bytes, const int32_t *indices, int64_t u,
+                         int32_t num_walks, int32_t num_steps, uint64_t state, int32_t *out,
+                         uint64_t *end_state_out, wj_stream_t stream);
+
+/* Distinct landings per anchor (counts_out[k] = |V_{lo+k}|).
+ * Replaces _kernels.count_distinct_all (_kernels.py:87-101), sampler.py:117-121. */
+int wj_rpe_count(const int32_t *walks, int64_t n_anchors, int32_t num_walks, int32_t num_steps,
+                 int64_t n_nodes, int32_t *counts_out, wj_stream_t stream);
+
+/* Per-anchor RPE index: sorted unique landing ids (uniq_x), packed positional
+ * count vector (uniq_key: count of step c in bits [c*cb, (c+1)*cb), cb =
+ * bits(M)), first-appearance flat position (uniq_first) and, per walk slot,
+ * the index of its node in the anchor's unique list (slot_idx[k, M*(L+1)]).
+ * Entries of anchor k live at [offsets[k], offsets[k+1]).
+ * Replaces _kernels.fill_distinct_all (_kernels.py:104-126), sampler.py:122-128. */
+int wj_rpe_fill(const int32_t *walks, int64_t n_anchors, int32_t num_walks, int32_t num_steps,
+                int64_t n_nodes, const int64_t *offsets, int32_t *uniq_x, uint64_t *uniq_key,
+                uint16_t *uniq_first, uint16_t *slot_idx, wj_stream_t stream);
+
+/* Global interning, phase 1: insert every entry's packed vector into an
+ * open-addressing table (table_keys zeroed, table_order set to all-ones,
+ * table_cap a power of two) keeping the minimum scan order
+ * ((anchor_base+k) << 16 | first).  *overflow_flag becomes nonzero if the
+ * table fills.  Phase 2 (rank by first occurrence) is host plumbing; phase 3
+ * is wj_intern_assign.  Together they replace the sequential
+ * _kernels.intern_rows (_kernels.py:137-171) / store.intern_vectors
+ * (store.py:107-121) and reproduce its ids exactly. */
+int wj_intern_insert(const uint64_t *uniq_key, const uint16_t *uniq_first, const int64_t *offsets,
+                     int64_t n_anchors, int64_t anchor_base, uint64_t *table_keys,
+                     uint64_t *table_order, int64_t table_cap, int32_t *overflow_flag,
+                     wj_stream_t stream);
+
+/* Global interning, phase 3: uniq_id[e] = table_ids[slot of uniq_key[e]]. */
+int wj_intern_assign(const uint64_t *uniq_key, int64_t n_entries, const uint64_t *table_keys,
+                     const int32_t *table_ids, int64_t table_cap, int32_t *uniq_id,
+                     wj_stream_t stream);
+
+/* Query-level join fused with densify.  queries [B, A] int64.  Any of the
+ * three outputs may be NULL:
+ *   walk_nodes_out [B, A*M, L+1] int32          (_kernels.py:231-233)
+ *   rpe_ids_out    [B, A*M*(L+1), A] int32      (_kernels.py:237-245)
+ *   dense_out      [B, A*M*(L+1), row_stride] of dense_dtype; columns
+ *                  [0, A*(L+1)) get table[rpe_id] (pipeline.py:178)
+ * table_keys [table_len] packed count vectors (id order, row 0 = 0).
+ * Replaces joiner.join_batch_arrays (joiner.py:53-71) + _kernels.join_fill
+ * (_kernels.py:209-245) + the densify of pipeline._dense_batch
+ * (pipeline.py:169-182). */
+int wj_join(const int64_t *queries, int64_t n_batch, int32_t arity, const int32_t *walks,
+            const int64_t *offsets, const int32_t *uniq_x, const int32_t *uniq_id,
+            const uint16_t *slot_idx, int32_t num_walks, int32_t num_steps, int32_t max_unique,
+            const uint64_t *table_keys, int64_t table_len, int32_t *walk_nodes_out,
+            int32_t *rpe_ids_out, void *dense_out, int32_t dense_dtype, int64_t row_stride,
+            wj_stream_t stream);
+
+/* Densify ids: out[i, :] = table[rpe_ids[i], :] (table [T, width] int32).
+ * Replaces joiner.gather_rpe (joiner.py:96-104); *bad_flag set if an id is
+ * out of range (the reference raises ValueError). */
+int wj_gather_rpe(const int32_t *rpe_ids, int64_t n_ids, const int32_t *table, int64_t table_len,
+                  int32_t width, void *out, int32_t dtype, int32_t *bad_flag, wj_stream_t stream);
+
+/* Export the reference per-node dictionaries bit-exactly (dict_keys
+ * pre-filled with -1, dict_vals with 0; cap_offsets from
+ * store.dict_capacities).  Replaces _kernels.build_dicts
+ * (_kernels.py:174-188), sampler.py:133-138. */
+int wj_export_dicts(const int64_t *offsets, const int32_t *uniq_x, const int32_t *uniq_id,
+                    const uint16_t *uniq_first, const uint16_t *slot_idx, int64_t n_anchors,
+                    int32_t num_walks, int32_t num_steps, const int64_t *cap_offsets,
+                    int32_t *dict_keys, int32_t *dict_vals, wj_stream_t stream);
+
+/* Point lookups out[i] = RPE id of x[i] relative to anchor u[i] (0 if
+ * absent).  Replaces store.get_rpe_id / _kernels.dict_get_one
+ * (store.py:160-164, _kernels.py:203-206). */
+int wj_lookup(const int64_t *u, const int64_t *x, int64_t count, const int64_t *offsets,
+              const int32_t *uniq_x, const int32_t *uniq_id, int32_t *out, wj_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* WALKJOIN_B200_H */

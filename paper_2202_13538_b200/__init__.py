@@ -1,0 +1,29 @@
+"""B200-native walk -> RPE -> join hot path of SUREL (reference package ``walkjoin``).
+
+Drop-in for the reference's hot-path API (/root/reference/pkg/src/walkjoin):
+``preprocess``, ``sample_walks``, ``compute_rpe``, ``get_rpe_id``,
+``join_batch_arrays``, ``join_query``, ``join_batch``, ``gather_rpe`` and the
+``_dense_batch`` call site (``dense_batch``), backed by hand-written sm_100a
+kernels behind the C ABI in include/walkjoin_b200.h.  There is no CPU
+fallback: every call needs the in-tree CUDA library and a CUDA device.
+"""
+
+from .graph import DeviceGraph, Graph, GraphFormatError, Query, load_edge_list, project_hyperedges
+from .sampler import RawRpeMap, WalkRng, WalkSet, compute_rpe, preprocess, sample_walks
+from .store import NodeEntry, RpeTable, StoreFormatError, SubgraphStore, dict_capacities, get_rpe_id
+from .joiner import JoinedQuery, dense_batch, gather_rpe, join_batch, join_batch_arrays, join_query
+from .encoder import AdamState, ModelParams, adam_step, backward, bce_loss, forward, init_params
+from .pipeline import TrainConfig, TrainStep, infer
+
+_dense_batch = dense_batch  # reference call-site name (pipeline.py:169)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "Graph", "DeviceGraph", "GraphFormatError", "Query", "load_edge_list", "project_hyperedges",
+    "WalkSet", "RawRpeMap", "WalkRng", "sample_walks", "compute_rpe", "preprocess",
+    "RpeTable", "NodeEntry", "SubgraphStore", "StoreFormatError", "dict_capacities", "get_rpe_id",
+    "JoinedQuery", "join_query", "join_batch", "join_batch_arrays", "gather_rpe", "dense_batch",
+    "ModelParams", "AdamState", "init_params", "forward", "backward", "bce_loss", "adam_step",
+    "TrainConfig", "TrainStep", "infer",
+]

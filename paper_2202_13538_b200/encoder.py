@@ -1,0 +1,224 @@
+"""The encoder that consumes the joined RPE tensor, in PyTorch on the device.
+
+Reference: /root/reference/pkg/src/walkjoin/encoder.py (float64 numpy MLP
+with hand-written backprop).  Architecture, init, loss and Adam are the
+reference's; the math is re-expressed for the GPU:
+
+* ``mode="reference"`` follows the reference op order literally
+  (x@W1+b1 -> ReLU -> dropout -> @W2+b2 -> mean over steps -> mean over
+  walks -> classifier), fp32 or fp64.
+* ``mode="pooled"`` (default) uses the exact identity that the row mean
+  commutes with the affine W2 layer (encoder.py:159-161): hq = mean_rows(a1)
+  @ W2 + b2, with the row mean accumulated in fp64.  Backward needs only the
+  per-query column scale g_b = dhq_b @ W2^T / rows, so no [rows, hidden]
+  gradient of W2 is ever formed.
+
+Dropout masks are drawn from a torch generator, not numpy PCG64, so training
+trajectories match the reference statistically, not bitwise.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+import torch
+
+TENSOR_ORDER = ("w1", "b1", "w2", "b2", "u1", "c1", "u2", "c2")
+
+
+@dataclass
+class ModelParams:
+    """Weights of the step encoder and classifier (encoder.py:32-63), device tensors."""
+
+    arity: int
+    walk_steps: int
+    hidden: int
+    feature_dim: int
+    dropout: float
+    tensors: dict
+    version: int = 0
+
+    @property
+    def d_in(self) -> int:
+        return self.arity * (self.walk_steps + 1) + self.feature_dim
+
+    def __getattr__(self, name):
+        if name in TENSOR_ORDER:
+            return self.__dict__["tensors"][name]
+        raise AttributeError(name)
+
+    def copy(self) -> "ModelParams":
+        return ModelParams(self.arity, self.walk_steps, self.hidden, self.feature_dim, self.dropout,
+                           {k: v.clone() for k, v in self.tensors.items()}, self.version)
+
+    def numpy(self) -> dict:
+        return {k: v.detach().double().cpu().numpy() for k, v in self.tensors.items()}
+
+
+def _glorot(rng, fan_in, fan_out):
+    a = math.sqrt(6.0 / (fan_in + fan_out))
+    return rng.uniform(-a, a, size=(fan_in, fan_out))
+
+
+def init_params(arity, walk_steps, hidden=64, feature_dim=0, dropout=0.1, seed=0,
+                device="cuda", dtype=torch.float32) -> ModelParams:
+    """Seeded glorot-uniform weights, zero biases -- same draws as encoder.py:87-117."""
+    rng = np.random.default_rng(seed)
+    d_in = arity * (walk_steps + 1) + feature_dim
+    host = {
+        "w1": _glorot(rng, d_in, hidden), "b1": np.zeros(hidden),
+        "w2": _glorot(rng, hidden, hidden), "b2": np.zeros(hidden),
+        "u1": _glorot(rng, hidden, hidden), "c1": np.zeros(hidden),
+        "u2": _glorot(rng, hidden, 1)[:, 0], "c2": np.zeros(1),
+    }
+    return ModelParams(arity, walk_steps, hidden, feature_dim, dropout,
+                       {k: torch.tensor(v, dtype=dtype, device=device) for k, v in host.items()})
+
+
+def params_from_numpy(arrays: dict, arity, walk_steps, dropout=0.0, device="cuda",
+                      dtype=torch.float32) -> ModelParams:
+    t = {k: torch.tensor(np.asarray(arrays[k]), dtype=dtype, device=device) for k in TENSOR_ORDER}
+    hidden = t["w1"].shape[1]
+    feature_dim = t["w1"].shape[0] - arity * (walk_steps + 1)
+    return ModelParams(arity, walk_steps, hidden, feature_dim, dropout, t)
+
+
+def dropout_mask(shape, keep: float, generator, device, dtype):
+    """Inverted-dropout mask {0, 1/keep} (encoder.py:157)."""
+    return (torch.rand(shape, generator=generator, device=device) < keep).to(dtype) / keep
+
+
+def forward(p: ModelParams, dense: torch.Tensor, training: bool = False,
+            generator: Optional[torch.Generator] = None, mode: str = "pooled",
+            drop_mask: Optional[torch.Tensor] = None):
+    """[B, rows, d_in] -> ([B] logits, cache) (encoder.py:126-180)."""
+    x = dense if dense.dim() == 3 else dense[None]
+    B, rows, d_in = x.shape
+    if d_in != p.d_in:
+        raise ValueError(f"input width {d_in} does not match model d_in {p.d_in}")
+    width = p.walk_steps + 1
+    if rows % width != 0:
+        raise ValueError(f"row count {rows} is not a multiple of m+1 = {width}")
+    t = p.tensors
+    dt = t["w1"].dtype
+    flat = x.reshape(B * rows, d_in)
+    if flat.dtype != dt:
+        flat = flat.to(dt)
+    z1 = torch.addmm(t["b1"], flat, t["w1"])
+    relu1 = z1 > 0
+    a1 = torch.relu_(z1)
+    mask = drop_mask
+    if mask is None and training and p.dropout > 0.0:
+        mask = dropout_mask(a1.shape, 1.0 - p.dropout, generator, a1.device, dt)
+    if mask is not None:
+        a1.mul_(mask.reshape(a1.shape))
+    if mode == "reference":
+        e = torch.addmm(t["b2"], a1, t["w2"])
+        walk_enc = e.reshape(B, rows // width, width, p.hidden).mean(dim=2)
+        hq = walk_enc.to(torch.float64).mean(dim=1).to(dt)
+        pooled = None
+    else:
+        pooled = a1.reshape(B, rows, p.hidden).sum(dim=1, dtype=torch.float64).div_(rows).to(dt)
+        hq = torch.addmm(t["b2"], pooled, t["w2"])
+    z2 = torch.addmm(t["c1"], hq, t["u1"])
+    relu2 = z2 > 0
+    a2 = torch.relu(z2)
+    logits = a2 @ t["u2"] + t["c2"][0]
+    cache = dict(x=flat, relu1=relu1, mask=mask, a1d=a1, pooled=pooled, hq=hq, relu2=relu2, a2=a2,
+                 logits=logits, rows=rows, B=B, mode=mode, version=p.version)
+    return logits, cache
+
+
+def bce_loss(logits: torch.Tensor, labels: torch.Tensor) -> torch.Tensor:
+    """Numerically stable mean BCE on the logit scale (encoder.py:183-188)."""
+    z = logits
+    return (torch.clamp_min(z, 0) - z * labels + torch.log1p(torch.exp(-z.abs()))).mean()
+
+
+def backward(p: ModelParams, cache: dict, labels: torch.Tensor) -> dict:
+    """Gradients of the mean BCE (encoder.py:200-233)."""
+    if cache["version"] != p.version:
+        raise ValueError("stale cache: params were updated after this forward pass")
+    t = p.tensors
+    logits = cache["logits"]
+    B, rows = cache["B"], cache["rows"]
+    y = labels.to(logits.dtype)
+    dlogit = (torch.sigmoid(logits) - y) / B
+    dc2 = dlogit.sum().reshape(1)
+    du2 = cache["a2"].t() @ dlogit
+    dz2 = torch.outer(dlogit, t["u2"]) * cache["relu2"]
+    dc1 = dz2.sum(0)
+    du1 = cache["hq"].t() @ dz2
+    dhq = dz2 @ t["u1"].t()
+    db2 = dhq.sum(0)
+    if cache["mode"] == "reference":
+        de = (dhq / rows).repeat_interleave(rows, dim=0)
+        dw2 = cache["a1d"].t() @ de
+        da1 = de @ t["w2"].t()
+    else:
+        dw2 = cache["pooled"].t() @ dhq
+        g = (dhq @ t["w2"].t()) / rows                       # [B, h], same for every row of b
+        da1 = g[:, None, :].expand(B, rows, p.hidden).reshape(B * rows, p.hidden)
+    dz1 = da1 * cache["relu1"]
+    if cache["mask"] is not None:
+        dz1 = dz1 * cache["mask"].reshape(dz1.shape)
+    db1 = dz1.sum(0)
+    dw1 = cache["x"].t() @ dz1
+    return {"w1": dw1, "b1": db1, "w2": dw2, "b2": db2, "u1": du1, "c1": dc1, "u2": du2, "c2": dc2}
+
+
+@dataclass
+class AdamState:
+    """First/second moments (encoder.py:66-84)."""
+
+    lr: float = 1e-3
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    step: int = 0
+    m: dict = field(default_factory=dict)
+    v: dict = field(default_factory=dict)
+
+    @classmethod
+    def for_params(cls, p: ModelParams, lr: float = 1e-3) -> "AdamState":
+        s = cls(lr=lr)
+        for k, v in p.tensors.items():
+            s.m[k] = torch.zeros_like(v)
+            s.v[k] = torch.zeros_like(v)
+        return s
+
+
+def adam_step(p: ModelParams, grads: dict, state: AdamState) -> None:
+    """Bias-corrected Adam, in place, reference op order (encoder.py:236-249)."""
+    state.step += 1
+    t = state.step
+    bc1 = 1.0 - state.beta1 ** t
+    bc2 = 1.0 - state.beta2 ** t
+    for name in TENSOR_ORDER:
+        g = grads[name]
+        tensor = p.tensors[name]
+        if g.shape != tensor.shape:
+            raise ValueError(f"gradient shape {tuple(g.shape)} != param shape {tuple(tensor.shape)} for {name}")
+        m, v = state.m[name], state.v[name]
+        m.mul_(state.beta1).add_(g, alpha=1.0 - state.beta1)
+        v.mul_(state.beta2).addcmul_(g, g, value=1.0 - state.beta2)
+        tensor.sub_(state.lr * (m / bc1) / ((v / bc2).sqrt_().add_(state.eps)))
+    p.version += 1
+
+
+def adam_step_graphable(p: ModelParams, grads: dict, state: AdamState, inv_bc: torch.Tensor) -> None:
+    """Adam with the bias corrections read from a device tensor
+    ``inv_bc = [1/(1-beta1^t), 1/(1-beta2^t)]`` that the host refreshes before
+    each replay, so the update can live inside a captured CUDA graph."""
+    for name in TENSOR_ORDER:
+        g = grads[name]
+        tensor = p.tensors[name]
+        m, v = state.m[name], state.v[name]
+        m.mul_(state.beta1).add_(g, alpha=1.0 - state.beta1)
+        v.mul_(state.beta2).addcmul_(g, g, value=1.0 - state.beta2)
+        mh = m * inv_bc[0]
+        vh = v * inv_bc[1]
+        tensor.sub_(state.lr * mh / (vh.sqrt_().add_(state.eps)))

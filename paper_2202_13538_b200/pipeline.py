@@ -1,0 +1,295 @@
+"""Training orchestration around the device hot path (reference pipeline.py).
+
+The batch plan (BFS mini-batches over query overlap + in-seed negatives,
+pipeline.py:54-166) stays on the host: it is sequential and tiny.  Each
+training step -- join+densify kernel, encoder forward, BCE, backward, Adam --
+runs on the device and is captured once per batch shape as a CUDA graph, so a
+step is one graph launch plus the H2D copy of the batch's query ids.
+"""
+
+from __future__ import annotations
+
+import logging
+import time
+from collections import deque
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import encoder as E
+from .joiner import dense_batch
+from .store import SubgraphStore
+
+logger = logging.getLogger(__name__)
+
+
+@dataclass
+class TrainConfig:
+    """pipeline.py:30-51 (same defaults)."""
+
+    batch_capacity: int = 1500
+    batch_size: int = 32
+    k_neg: int = 50
+    lr: float = 1e-3
+    max_epochs: int = 50
+    patience: int = 5
+    seed: int = 0
+    threads: int = 1
+    hidden_dim: int = 64
+    dropout: float = 0.1
+    metric: str = "auc"
+    use_features: bool = False
+
+    def __post_init__(self):
+        if self.batch_capacity < 1 or self.batch_size < 1 or self.k_neg < 1:
+            raise ValueError("batch_capacity, batch_size, and k_neg must be >= 1")
+        if self.metric not in ("auc", "mrr"):
+            raise ValueError(f"unknown validation metric {self.metric!r}")
+
+
+class QueryOverlapIndex:
+    """node id -> training queries containing it (pipeline.py:54-69), CSR form."""
+
+    def __init__(self, queries):
+        q = np.asarray([getattr(x, "nodes", x) for x in queries], dtype=np.int64)
+        if q.ndim != 2:
+            raise ValueError("queries must share one arity")
+        self.queries = q
+        flat = q.reshape(-1)
+        qid = np.repeat(np.arange(q.shape[0], dtype=np.int64), q.shape[1])
+        order = np.argsort(flat, kind="stable")  # per node, query ids ascending
+        self._qids = qid[order]
+        self.nodes, starts, counts = np.unique(flat[order], return_index=True, return_counts=True)
+        self._start = dict(zip(self.nodes.tolist(), starts.tolist()))
+        self._count = dict(zip(self.nodes.tolist(), counts.tolist()))
+
+    def queries_of(self, u: int):
+        s = self._start.get(u)
+        if s is None:
+            return []
+        return self._qids[s: s + self._count[u]].tolist()
+
+    def __len__(self) -> int:
+        return int(self.nodes.shape[0])
+
+
+def canonical_nodes(nodes) -> tuple:
+    return tuple(sorted(int(v) for v in nodes))
+
+
+def sample_minibatch(index: QueryOverlapIndex, queries, cfg: TrainConfig, rng: np.random.Generator,
+                     n_seeds: Optional[int] = None, exact: bool = False):
+    """BFS over query-sharing neighbours (pipeline.py:77-129).
+
+    ``exact=True`` draws the seed nodes with ``rng.choice(..., replace=False)``
+    exactly like the reference (a full permutation of the node list per
+    batch); the default draws the same uniform distinct subset by rejection,
+    which is O(n_seeds)."""
+    if len(index) == 0:
+        raise ValueError("empty training query set")
+    if n_seeds is None:
+        n_seeds = min(16, cfg.batch_capacity)
+    n_seeds = min(n_seeds, len(index.nodes))
+    if exact:
+        seeds = rng.choice(index.nodes, size=n_seeds, replace=False)
+    else:
+        picked: list = []
+        seen: set = set()
+        while len(picked) < n_seeds:
+            for i in rng.integers(0, len(index.nodes), size=2 * (n_seeds - len(picked))).tolist():
+                if i not in seen and len(picked) < n_seeds:
+                    seen.add(i)
+                    picked.append(i)
+        seeds = index.nodes[np.asarray(picked, dtype=np.int64)]
+    qarr = index.queries
+    seed_list, in_seed, batch, in_batch, queue = [], set(), [], set(), deque()
+    for s in seeds.tolist():
+        if s not in in_seed:
+            in_seed.add(s)
+            seed_list.append(s)
+            queue.append(s)
+    full = False
+    while queue and not full:
+        u = queue.popleft()
+        for qid in index.queries_of(u):
+            if qid in in_batch:
+                continue
+            if len(batch) >= cfg.batch_size:
+                full = True
+                break
+            in_batch.add(qid)
+            batch.append(qid)
+            for w in qarr[qid].tolist():
+                if w not in in_seed:
+                    if len(seed_list) >= cfg.batch_capacity:
+                        full = True
+                        break
+                    in_seed.add(w)
+                    seed_list.append(w)
+                    queue.append(w)
+            if full:
+                break
+    return seed_list, batch
+
+
+class PositiveFilter:
+    """Membership test of canonical node tuples against the positive set,
+    vectorised over sorted packed keys (pipeline.py:278-280)."""
+
+    def __init__(self, tuples: np.ndarray, num_nodes: int):
+        t = np.sort(np.asarray(tuples, dtype=np.int64), axis=1)
+        self.n = int(num_nodes)
+        self.keys = np.unique(self._pack(t))
+
+    def _pack(self, t: np.ndarray) -> np.ndarray:
+        k = np.zeros(t.shape[0], dtype=np.int64)
+        for c in range(t.shape[1]):
+            k = k * self.n + t[:, c]
+        return k
+
+    def contains(self, rows: np.ndarray) -> np.ndarray:
+        k = self._pack(np.sort(rows, axis=1))
+        pos = np.searchsorted(self.keys, k)
+        pos = np.minimum(pos, len(self.keys) - 1)
+        return self.keys[pos] == k if len(self.keys) else np.zeros(len(k), bool)
+
+
+def sample_negatives(seed_set: Sequence[int], arity: int, count: int, positive_filter,
+                     rng: np.random.Generator) -> np.ndarray:
+    """Uniform distinct-node tuples inside the seed set, rejected against the
+    positives (pipeline.py:132-166).  Vectorised per chunk with the same rng
+    draws and acceptance order as the reference loop, so for the same
+    generator state it returns the same queries.  ``positive_filter`` is a
+    PositiveFilter or a set of canonical tuples."""
+    nodes = np.asarray(list(seed_set), dtype=np.int64)
+    if nodes.shape[0] < arity:
+        raise ValueError(f"seed set of {nodes.shape[0]} nodes cannot host arity-{arity} negatives")
+    out = []
+    have = 0
+    budget = 1000 * count
+    while have < count:
+        chunk = min(max(2 * (count - have), 64), budget)
+        if chunk <= 0:
+            break
+        draws = rng.integers(0, nodes.shape[0], size=(chunk, arity))
+        budget -= chunk
+        picked = nodes[draws]
+        s = np.sort(picked, axis=1)
+        ok = np.all(s[:, 1:] != s[:, :-1], axis=1) if arity > 1 else np.ones(chunk, bool)
+        if isinstance(positive_filter, PositiveFilter):
+            ok &= ~positive_filter.contains(picked)
+        else:
+            ok &= np.array([tuple(r) not in positive_filter for r in s.tolist()], bool)
+        acc = picked[ok][: count - have]
+        out.append(acc)
+        have += acc.shape[0]
+        if budget <= 0 and have < count:
+            raise ValueError(f"negative sampling budget exhausted after producing {have}/{count} queries")
+    return np.concatenate(out) if out else np.empty((0, arity), np.int64)
+
+
+def make_batch(index, positives: np.ndarray, pos_filter, cfg: TrainConfig, rng, exact=False):
+    """One batch of query ids + labels (pipeline.py:293-304)."""
+    seeds, ids = sample_minibatch(index, positives, cfg, rng, exact=exact)
+    pos = positives[np.asarray(ids, dtype=np.int64)]
+    negs = sample_negatives(seeds, positives.shape[1], cfg.k_neg * len(ids), pos_filter, rng)
+    q = np.concatenate([pos, negs]).astype(np.int64)
+    labels = np.concatenate([np.ones(len(ids)), np.zeros(len(negs))]).astype(np.float32)
+    return q, labels
+
+
+class TrainStep:
+    """join+densify -> forward -> BCE -> backward -> Adam on the device,
+    captured as one CUDA graph per batch shape (``use_graph``)."""
+
+    def __init__(self, store: SubgraphStore, params: E.ModelParams, state: E.AdamState,
+                 dense_dtype=torch.float32, mode: str = "pooled", use_graph: bool = True):
+        self.store, self.params, self.state = store, params, state
+        self.dense_dtype, self.mode, self.use_graph = dense_dtype, mode, use_graph
+        self.dev = store.device
+        self.inv_bc = torch.ones(2, dtype=params.w1.dtype, device=self.dev)
+        self._host_bc = torch.ones(2, dtype=params.w1.dtype).pin_memory()
+        self._graphs: dict = {}
+
+    def _body(self, q, y, dense, inv_bc):
+        dense_batch(self.store, q, dtype=self.dense_dtype, out=dense, validate=False)
+        logits, cache = E.forward(self.params, dense, training=True, mode=self.mode)
+        loss = E.bce_loss(logits, y)
+        grads = E.backward(self.params, cache, y)
+        E.adam_step_graphable(self.params, grads, self.state, inv_bc)
+        return loss
+
+    def _prepare_bc(self):
+        self.state.step += 1
+        t = self.state.step
+        self._host_bc[0] = 1.0 / (1.0 - self.state.beta1 ** t)
+        self._host_bc[1] = 1.0 / (1.0 - self.state.beta2 ** t)
+        self.inv_bc.copy_(self._host_bc, non_blocking=True)
+
+    def __call__(self, q: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
+        """q: [B, A] int64 device ids, y: [B] labels (device).  Returns the loss (device)."""
+        B, A = q.shape
+        self._prepare_bc()
+        if not self.use_graph:
+            dense = torch.empty((B, A * self.store.landings, A * self.store.width),
+                                dtype=self.dense_dtype, device=self.dev)
+            out = self._body(q, y.to(self.params.w1.dtype), dense, self.inv_bc)
+            self.params.version += 1
+            return out
+        key = (B, A)
+        g = self._graphs.get(key)
+        if g is None:
+            g = self._capture(B, A)
+            self._graphs[key] = g
+        g["q"].copy_(q, non_blocking=True)
+        g["y"].copy_(y, non_blocking=True)
+        g["graph"].replay()
+        self.params.version += 1
+        return g["loss"]
+
+    def _capture(self, B, A):
+        dev = self.dev
+        q = torch.zeros((B, A), dtype=torch.int64, device=dev)
+        q[:, :] = torch.arange(A, device=dev)[None, :] % max(self.store.num_nodes, 1)
+        y = torch.zeros(B, dtype=self.params.w1.dtype, device=dev)
+        dense = torch.empty((B, A * self.store.landings, A * self.store.width), dtype=self.dense_dtype,
+                            device=dev)
+        # warm up on a side stream (allocator + cuBLAS handles), then capture;
+        # params / Adam state are snapshotted so warm-up leaves no trace
+        snap_p = {k: v.clone() for k, v in self.params.tensors.items()}
+        snap_m = {k: v.clone() for k, v in self.state.m.items()}
+        snap_v = {k: v.clone() for k, v in self.state.v.items()}
+        s = torch.cuda.Stream(dev)
+        s.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(s):
+            for _ in range(2):
+                self._body(q, y, dense, self.inv_bc)
+        torch.cuda.current_stream(dev).wait_stream(s)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            loss = self._body(q, y, dense, self.inv_bc)
+        for k in snap_p:
+            self.params.tensors[k].copy_(snap_p[k])
+            self.state.m[k].copy_(snap_m[k])
+            self.state.v[k].copy_(snap_v[k])
+        return {"graph": graph, "q": q, "y": y, "dense": dense, "loss": loss}
+
+
+def infer(store: SubgraphStore, params: E.ModelParams, queries, threads: int = 1, features=None,
+          chunk: int = 2048) -> np.ndarray:
+    """Sigmoid scores, input order (pipeline.py:329-355)."""
+    if len(queries) == 0:
+        return np.empty(0, dtype=np.float64)
+    rows = np.asarray([getattr(q, "nodes", q) for q in queries], dtype=np.int64)
+    if rows.shape[1] != params.arity:
+        raise ValueError(f"queries have arity {rows.shape[1]} but model was trained with arity {params.arity}")
+    out = []
+    q_all = torch.from_numpy(rows).to(store.device)
+    for lo in range(0, rows.shape[0], chunk):
+        dense = dense_batch(store, q_all[lo: lo + chunk], features=features,
+                            dtype=params.w1.dtype)
+        logits, _ = E.forward(params, dense, training=False)
+        out.append(torch.sigmoid(logits.double()))
+    return torch.cat(out).cpu().numpy()

@@ -1,0 +1,254 @@
+"""HBM-resident subgraph store with the reference SubgraphStore surface.
+
+Reference: /root/reference/pkg/src/walkjoin/store.py.  The reference store
+is walks + a global table of deduplicated count vectors + one open-addressing
+dict per node (store.py:58-104).  The device store keeps, per anchor u,
+
+* ``walks``      [n, M, L+1] int32          -- the walk table (store.walks)
+* ``offsets``    [n+1] int64                -- entries of u at [off[u], off[u+1])
+* ``uniq_x``     [E] int32, sorted per anchor -- distinct landings (V_u)
+* ``uniq_id``    [E] int32                  -- global RPE id of (u, x)
+* ``uniq_first`` [E] uint16                 -- first-appearance flat slot
+* ``slot_idx``   [n, M*(L+1)] uint16         -- per walk slot, index into u's list
+* ``table_keys`` [T] int64 (u64 bits)        -- packed count vector of each id
+
+which replaces the hash dicts by a compact sorted index (the join binary
+searches it in shared memory).  The reference's host arrays (``walks``,
+``table``, ``dict_offsets`` / ``dict_keys`` / ``dict_vals``) are materialised
+lazily and bit-exactly on first access -- the dicts by the wj_export_dicts
+kernel -- so code written against the reference store runs unchanged.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+
+
+class StoreFormatError(RuntimeError):
+    """Wrong magic / version / length in a store file (store.py:29-30)."""
+
+
+@dataclass
+class RpeTable:
+    """Deduplicated positional count vectors; row 0 is the zero sentinel (store.py:33-46)."""
+
+    vectors: np.ndarray  # [T, L+1] int32
+
+    def __post_init__(self):
+        self.vectors.setflags(write=False)
+
+    def __len__(self) -> int:
+        return self.vectors.shape[0]
+
+    def __getitem__(self, idx):
+        return self.vectors[idx]
+
+
+@dataclass
+class NodeEntry:
+    """One node's walks and its node-id -> RPE-id dictionary (store.py:49-55)."""
+
+    anchor: int
+    walks: np.ndarray
+    dict: dict
+
+
+def dict_capacities(counts) -> np.ndarray:
+    """Smallest power of two >= max(2, 2*count) per node (store.py:124-131)."""
+    need = np.maximum(2 * np.asarray(counts, dtype=np.int64), 2)
+    caps = np.int64(1) << np.ceil(np.log2(need)).astype(np.int64)
+    caps[caps < need] <<= 1
+    shrink = (caps >> 1) >= need
+    caps[shrink] >>= 1
+    return caps
+
+
+def count_bits(num_walks: int) -> int:
+    return max(1, int(num_walks).bit_length())
+
+
+def unpack_table(table_keys: torch.Tensor, num_walks: int, width: int) -> torch.Tensor:
+    """[T] packed vectors -> [T, width] int32 counts (field c at bits c*cb)."""
+    cb = count_bits(num_walks)
+    shifts = torch.arange(width, device=table_keys.device, dtype=torch.int64) * cb
+    return ((table_keys[:, None] >> shifts[None, :]) & ((1 << cb) - 1)).to(torch.int32)
+
+
+class SubgraphStore:
+    """Device store; attribute surface of the reference SubgraphStore."""
+
+    def __init__(self, num_nodes, num_walks, walk_steps, seed, walks_d, offsets_d, uniq_x_d,
+                 uniq_id_d, uniq_first_d, slot_idx_d, table_keys_d, max_unique, id_map=None,
+                 anchor_counts=None):
+        self.num_nodes = int(num_nodes)
+        self.num_walks = int(num_walks)
+        self.walk_steps = int(walk_steps)
+        self.seed = int(seed)
+        self.id_map = id_map
+        self.walks_d = walks_d
+        self.offsets_d = offsets_d
+        self.uniq_x_d = uniq_x_d
+        self.uniq_id_d = uniq_id_d
+        self.uniq_first_d = uniq_first_d
+        self.slot_idx_d = slot_idx_d
+        self.table_keys_d = table_keys_d
+        self.max_unique = int(max_unique)
+        self.device = walks_d.device
+        self._anchor_counts = anchor_counts
+        self._cache: dict = {}
+
+    # ---------------------------------------------------------- shapes --
+    @property
+    def width(self) -> int:
+        return self.walk_steps + 1
+
+    @property
+    def landings(self) -> int:
+        return self.num_walks * self.width
+
+    @property
+    def walk_slot_count(self) -> int:
+        return self.num_nodes * self.num_walks * (self.walk_steps + 1)
+
+    @property
+    def num_entries(self) -> int:
+        return int(self.uniq_x_d.numel())
+
+    # ------------------------------------------------ host materialisers --
+    def _host(self, key, fn):
+        if key not in self._cache:
+            arr = fn()
+            arr.setflags(write=False)
+            self._cache[key] = arr
+        return self._cache[key]
+
+    @property
+    def walks(self) -> np.ndarray:
+        return self._host("walks", lambda: self.walks_d.cpu().numpy())
+
+    @property
+    def table_d(self) -> torch.Tensor:
+        if "table_d" not in self._cache:
+            self._cache["table_d"] = unpack_table(self.table_keys_d, self.num_walks, self.width)
+        return self._cache["table_d"]
+
+    @property
+    def table(self) -> RpeTable:
+        if "table" not in self._cache:
+            self._cache["table"] = RpeTable(self.table_d.cpu().numpy())
+        return self._cache["table"]
+
+    def anchor_counts(self) -> torch.Tensor:
+        if self._anchor_counts is None:
+            self._anchor_counts = (self.offsets_d[1:] - self.offsets_d[:-1]).to(torch.int64)
+        return self._anchor_counts
+
+    def _export_dicts(self):
+        counts = self.anchor_counts().cpu().numpy()
+        caps = dict_capacities(counts)
+        cap_offsets = np.zeros(self.num_nodes + 1, np.int64)
+        np.cumsum(caps, out=cap_offsets[1:])
+        dev = self.device
+        cap_d = torch.from_numpy(cap_offsets).to(dev)
+        keys = torch.full((int(cap_offsets[-1]),), -1, dtype=torch.int32, device=dev)
+        vals = torch.zeros(int(cap_offsets[-1]), dtype=torch.int32, device=dev)
+        _lib.call("wj_export_dicts", _lib.ptr(self.offsets_d), _lib.ptr(self.uniq_x_d),
+                  _lib.ptr(self.uniq_id_d), _lib.ptr(self.uniq_first_d), _lib.ptr(self.slot_idx_d),
+                  self.num_nodes, self.num_walks, self.walk_steps, _lib.ptr(cap_d), _lib.ptr(keys),
+                  _lib.ptr(vals), _lib.stream_handle(dev))
+        for k, a in (("dict_offsets", cap_offsets), ("dict_keys", keys.cpu().numpy()),
+                     ("dict_vals", vals.cpu().numpy())):
+            a.setflags(write=False)
+            self._cache[k] = a
+
+    @property
+    def dict_offsets(self) -> np.ndarray:
+        if "dict_offsets" not in self._cache:
+            self._export_dicts()
+        return self._cache["dict_offsets"]
+
+    @property
+    def dict_keys(self) -> np.ndarray:
+        if "dict_keys" not in self._cache:
+            self._export_dicts()
+        return self._cache["dict_keys"]
+
+    @property
+    def dict_vals(self) -> np.ndarray:
+        if "dict_vals" not in self._cache:
+            self._export_dicts()
+        return self._cache["dict_vals"]
+
+    def entry(self, u: int) -> NodeEntry:
+        """Walks + {node: rpe id} of anchor u (store.py:81-91).  The dict is
+        the anchor's reference hash dict, exported on device, iterated in
+        slot order exactly like the reference."""
+        self._check_node(u)
+        if "dict_keys" in self._cache:
+            lo, hi = self.dict_offsets[u], self.dict_offsets[u + 1]
+            keys, vals = self.dict_keys[lo:hi], self.dict_vals[lo:hi]
+        else:
+            dev = self.device
+            count = int((self.offsets_d[u + 1] - self.offsets_d[u]).item())
+            cap = int(dict_capacities([count])[0])
+            cap_d = torch.tensor([0, cap], dtype=torch.int64, device=dev)
+            kd = torch.full((cap,), -1, dtype=torch.int32, device=dev)
+            vd = torch.zeros(cap, dtype=torch.int32, device=dev)
+            _lib.call("wj_export_dicts", self.offsets_d.data_ptr() + 8 * u,
+                      _lib.ptr(self.uniq_x_d), _lib.ptr(self.uniq_id_d),
+                      _lib.ptr(self.uniq_first_d), self.slot_idx_d.data_ptr() + 2 * u * self.landings,
+                      1, self.num_walks, self.walk_steps, _lib.ptr(cap_d), _lib.ptr(kd),
+                      _lib.ptr(vd), _lib.stream_handle(dev))
+            keys, vals = kd.cpu().numpy(), vd.cpu().numpy()
+        filled = keys != -1
+        return NodeEntry(anchor=u, walks=self.walks_d[u].cpu().numpy(),
+                         dict={int(k): int(v) for k, v in zip(keys[filled], vals[filled])})
+
+    def byte_sizes(self) -> dict:
+        """Reference-format sizes (store.py:93-100) plus the device index."""
+        counts = self.anchor_counts().cpu().numpy()
+        dict_slots = int(dict_capacities(counts).sum())
+        sizes = {
+            "walks": self.walk_slot_count * 4,
+            "table": int(self.table_keys_d.numel()) * self.width * 4,
+            "dicts": dict_slots * 8 + (self.num_nodes + 1) * 8,
+        }
+        sizes["total"] = sum(sizes.values())
+        sizes["device_index"] = sum(int(t.numel()) * t.element_size() for t in (
+            self.offsets_d, self.uniq_x_d, self.uniq_id_d, self.uniq_first_d, self.slot_idx_d,
+            self.table_keys_d))
+        return sizes
+
+    def _check_node(self, u: int):
+        if not 0 <= u < self.num_nodes:
+            raise ValueError(f"node id {u} out of range [0, {self.num_nodes})")
+
+
+def get_rpe_id(store: SubgraphStore, u: int, x: int) -> int:
+    """RPE id of x relative to anchor u, 0 if absent (store.py:160-164)."""
+    store._check_node(u)
+    dev = store.device
+    ut = torch.tensor([int(u)], dtype=torch.int64, device=dev)
+    xt = torch.tensor([int(x)], dtype=torch.int64, device=dev)
+    out = torch.empty(1, dtype=torch.int32, device=dev)
+    _lib.call("wj_lookup", _lib.ptr(ut), _lib.ptr(xt), 1, _lib.ptr(store.offsets_d),
+              _lib.ptr(store.uniq_x_d), _lib.ptr(store.uniq_id_d), _lib.ptr(out),
+              _lib.stream_handle(dev))
+    return int(out.item())
+
+
+def get_rpe_ids(store: SubgraphStore, u: torch.Tensor, x: torch.Tensor) -> torch.Tensor:
+    """Batched device lookups (no range check on u beyond the caller's)."""
+    u = u.to(store.device, torch.int64).contiguous()
+    x = x.to(store.device, torch.int64).contiguous()
+    out = torch.empty(u.shape, dtype=torch.int32, device=store.device)
+    _lib.call("wj_lookup", _lib.ptr(u), _lib.ptr(x), u.numel(), _lib.ptr(store.offsets_d),
+              _lib.ptr(store.uniq_x_d), _lib.ptr(store.uniq_id_d), _lib.ptr(out),
+              _lib.stream_handle(store.device))
+    return out

@@ -1,0 +1,260 @@
+"""Parity of the CUDA path (through the C ABI) with the reference fixtures and
+the CPU oracle.  Bit-exact for walks / RPE index / table / dicts / join /
+dense; encoder logits within 1e-5 relative (north_star tolerance)."""
+
+import numpy as np
+import pytest
+
+from conftest import golden_cases, load_golden
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def wj():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2202_13538_b200 as m
+
+    m._lib.load()
+    return m
+
+
+def _graph(wj, g):
+    return wj.Graph(int(g["n"]), g["idxptr"].astype(np.int64), g["indices"].astype(np.int32))
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_store_bit_exact_vs_reference(wj, name):
+    g = load_golden(name)
+    store = wj.preprocess(_graph(wj, g), int(g["M"]), int(g["L"]), int(g["seed"]))
+    np.testing.assert_array_equal(store.walks, g["walks"])
+    np.testing.assert_array_equal(store.table.vectors, g["table"])
+    np.testing.assert_array_equal(store.dict_offsets, g["dict_offsets"])
+    np.testing.assert_array_equal(store.dict_keys, g["dict_keys"])
+    np.testing.assert_array_equal(store.dict_vals, g["dict_vals"])
+    assert store.walk_slot_count == int(g["n"]) * int(g["M"]) * (int(g["L"]) + 1)
+
+
+@pytest.mark.parametrize("name", [c for c in golden_cases() if "queries" in load_golden(c)])
+def test_join_dense_bit_exact_vs_reference(wj, name):
+    g = load_golden(name)
+    store = wj.preprocess(_graph(wj, g), int(g["M"]), int(g["L"]), int(g["seed"]))
+    wn, ri = wj.join_batch_arrays(store, g["queries"])
+    np.testing.assert_array_equal(wn, g["walk_nodes"])
+    np.testing.assert_array_equal(ri, g["rpe_ids"])
+    dense = wj.dense_batch(store, g["queries"])
+    assert dense.dtype == np.float64
+    np.testing.assert_array_equal(dense, g["dense"])
+    # device path, every dense dtype (counts are exact in all of them for M <= 256)
+    qd = torch.from_numpy(g["queries"]).cuda()
+    for dt in (torch.float32, torch.float64, torch.bfloat16, torch.float16):
+        if dt in (torch.bfloat16,) and int(g["M"]) > 256:
+            continue
+        dd = wj.dense_batch(store, qd, dtype=dt)
+        np.testing.assert_array_equal(dd.double().cpu().numpy(), g["dense"])
+    for b in range(g["queries"].shape[0]):
+        jq = wj.join_query(store, tuple(int(v) for v in g["queries"][b]))
+        np.testing.assert_array_equal(wj.gather_rpe(store.table, jq), g["dense"][b])
+
+
+@pytest.mark.parametrize("name", [c for c in golden_cases() if "logits" in load_golden(c)])
+@pytest.mark.parametrize("mode", ["pooled", "reference"])
+def test_encoder_logits_and_grads(wj, name, mode):
+    g = load_golden(name)
+    A, L = g["queries"].shape[1], int(g["L"])
+    p = wj.encoder.params_from_numpy({k: g["p_" + k] for k in wj.encoder.TENSOR_ORDER}, A, L)
+    dense = torch.from_numpy(g["dense"]).cuda()
+    logits, cache = wj.forward(p, dense, training=False, mode=mode)
+    ref = g["logits"]
+    tol = 1e-5 * max(np.abs(ref).max(), 1e-3)
+    np.testing.assert_allclose(logits.double().cpu().numpy(), ref, rtol=1e-5, atol=tol)
+    labels = torch.from_numpy(g["labels"]).cuda()
+    assert abs(float(wj.bce_loss(logits.double(), labels)) - float(g["loss"])) < 1e-5 * abs(float(g["loss"]))
+    grads = wj.backward(p, cache, labels)
+    for k in wj.encoder.TENSOR_ORDER:
+        r = g["g_" + k]
+        np.testing.assert_allclose(grads[k].double().cpu().numpy(), r, rtol=1e-4,
+                                   atol=1e-4 * max(np.abs(r).max(), 1e-12))
+    state = wj.AdamState.for_params(p)
+    wj.adam_step(p, grads, state)
+    for k in wj.encoder.TENSOR_ORDER:
+        np.testing.assert_allclose(p.tensors[k].double().cpu().numpy(), g["p2_" + k], rtol=1e-5, atol=1e-6)
+
+
+def test_spec_examples(wj, golden_meta):
+    tri = wj.load_edge_list(["0 1", "1 2", "0 2"])
+    rng = wj.WalkRng.for_node(42, 0)
+    assert rng.state == 0xBDD732262FEB6E95
+    ws = wj.sample_walks(tri, 0, 4, 3, rng)
+    assert ws.walks.tolist() == golden_meta["triangle_walks_u0"]
+    assert rng.state == golden_meta["triangle_end_state"]
+    raw = wj.compute_rpe(ws)
+    assert list(raw.entries) == [int(k) for k in golden_meta["triangle_rpe_u0"]]
+    assert {str(k): v.tolist() for k, v in raw.entries.items()} == golden_meta["triangle_rpe_u0"]
+    path = wj.load_edge_list(["0 1"])
+    s = wj.preprocess(path, 2, 2, seed=5)
+    assert wj.get_rpe_id(s, 0, 1) == 2 and wj.get_rpe_id(s, 0, 99) == 0
+    with pytest.raises(ValueError):
+        wj.get_rpe_id(s, 2, 0)
+    assert s.entry(0).dict == {0: 1, 1: 2} and s.entry(1).dict == {0: 2, 1: 1}
+    jq = wj.join_query(s, (0, 1))
+    assert jq.walk_nodes.tolist() == [[0, 1, 0], [0, 1, 0], [1, 0, 1], [1, 0, 1]]
+    assert wj.gather_rpe(s.table, jq)[0].tolist() == [2, 0, 2, 0, 2, 0]
+    assert wj.join_batch(s, []) == []
+    with pytest.raises(ValueError):
+        wj.join_batch(s, [(0, 1), (0,)])
+    with pytest.raises(ValueError):
+        wj.join_query(s, (0, 7))
+    # isolated node, M=1, m=1 -> T = [[0,0],[1,1]]
+    iso = wj.Graph.from_edges(np.empty((0, 2), np.int64), 1)
+    s1 = wj.preprocess(iso, 1, 1, seed=9)
+    assert s1.table.vectors.tolist() == [[0, 0], [1, 1]] and s1.walks.tolist() == [[[0, 0]]]
+    with pytest.raises(ValueError):
+        wj.preprocess(path, 0, 2, seed=1)
+
+
+def _er(n, m, seed, isolated_frac=0.0):
+    rng = np.random.default_rng(seed)
+    import paper_2202_13538_b200 as wjm
+
+    hi = int(n * (1 - isolated_frac))
+    pairs = rng.integers(0, hi, size=(m, 2))
+    return wjm.Graph.from_edges(pairs, n)
+
+
+@pytest.mark.parametrize("n,m,M,L,seed", [
+    (10_000, 100_000, 50, 3, 3),     # C1 shape
+    (3_000, 6_000, 200, 4, 1),       # sparse, M=200 L=4 (citation2 M/L)
+    (2_000, 40_000, 100, 3, 7),      # dense, tags-math M/L
+    (1_500, 3_000, 400, 2, 2),       # M=400 L=2 (paper's vessel / collab setting, uint16-class counts)
+])
+def test_store_and_join_vs_oracle(wj, n, m, M, L, seed):
+    from oracle import core
+
+    g = _er(n, m, seed, isolated_frac=0.05)
+    s = wj.preprocess(g, M, L, seed)
+    r = core.preprocess(g.idxptr, g.indices, M, L, seed)
+    np.testing.assert_array_equal(s.walks, r.walks)
+    np.testing.assert_array_equal(s.table.vectors, r.table)
+    np.testing.assert_array_equal(s.dict_keys, r.dict_keys)
+    np.testing.assert_array_equal(s.dict_vals, r.dict_vals)
+    rng = np.random.default_rng(seed)
+    for A in (2, 3):
+        q = np.stack([rng.choice(n, A, replace=False) for _ in range(64)]).astype(np.int64)
+        wn, ri = wj.join_batch_arrays(s, q)
+        wr, rr = core.join_batch_arrays(r, q)
+        np.testing.assert_array_equal(wn, wr)
+        np.testing.assert_array_equal(ri, rr)
+    qd = torch.from_numpy(q).cuda()
+    dd = wj.dense_batch(s, qd, dtype=torch.float32).double().cpu().numpy()
+    np.testing.assert_array_equal(dd, core.dense_batch(r, q))
+
+
+def test_directed_dead_end_fixup(wj):
+    """Non-symmetric CSR: a mid-walk dead end consumes no draw, so later walks
+    shift; the device re-samples such anchors sequentially (bit-exact)."""
+    from oracle import core
+
+    rng = np.random.default_rng(5)
+    n = 400
+    deg = rng.integers(0, 4, size=n)
+    idxptr = np.zeros(n + 1, np.int64)
+    np.cumsum(deg, out=idxptr[1:])
+    indices = np.concatenate([np.sort(rng.choice(n, d, replace=False)) for d in deg]).astype(np.int32)
+    g = wj.Graph(n, idxptr, indices)
+    s = wj.preprocess(g, 30, 4, 99)
+    r = core.preprocess(idxptr, indices, 30, 4, 99)
+    np.testing.assert_array_equal(s.walks, r.walks)
+    np.testing.assert_array_equal(s.table.vectors, r.table)
+    np.testing.assert_array_equal(s.dict_vals, r.dict_vals)
+    for u in range(0, n, 37):
+        st = core.node_stream_state(7, u) ^ 0x1234
+        ws = wj.sample_walks(g, u, 9, 3, wj.WalkRng(st))
+        w_r, _ = core.sample_walks(idxptr, indices, u, 9, 3, st)
+        np.testing.assert_array_equal(ws.walks, w_r)
+
+
+def test_properties_at_collab_scale(wj):
+    """Size-independent properties at C2 scale (235K nodes, M=200, L=4)."""
+    dev = torch.device("cuda")
+    split = wj.graph.synthetic_link_graph(235_868, 1_285_465, 0.05, seed=1, device=dev)
+    g = split.walk_graph
+    s = wj.preprocess(g, 200, 4, 3)
+    n, M, W = g.num_nodes, 200, 5
+    walks = s.walks_d
+    # column 0 is the anchor
+    assert torch.equal(walks[:, :, 0], torch.arange(n, device=dev, dtype=torch.int32)[:, None].expand(n, M))
+    # every step is an edge (or a repeat at an isolated anchor)
+    ip = g.idxptr.long()
+    deg = ip[1:] - ip[:-1]
+    a = walks[:, :, :-1].reshape(-1).long()
+    b = walks[:, :, 1:].reshape(-1).long()
+    iso = deg[a] == 0
+    assert torch.all(a[iso] == b[iso])
+    ka = a[~iso][:5_000_000]
+    kb = b[~iso][:5_000_000]
+    key_e = ip.new_tensor(0)
+    lo = ip[ka]
+    hi = ip[ka + 1]
+    # binary search kb in the sorted neighbour row of ka
+    idx = g.indices.long()
+    left, right = lo.clone(), hi.clone()
+    for _ in range(32):
+        mid = (left + right) // 2
+        go = (left < right) & (idx[mid.clamp(max=idx.numel() - 1)] < kb)
+        left = torch.where(go, mid + 1, left)
+        right = torch.where(go | (left >= right), right, mid)
+    assert torch.all(idx[left.clamp(max=idx.numel() - 1)] == kb)
+    # RPE mass: every anchor's count vectors sum to M in every column
+    tab = s.table_d.long()
+    sums = torch.zeros((n, W), dtype=torch.int64, device=dev)
+    owner = torch.repeat_interleave(torch.arange(n, device=dev), s.anchor_counts())
+    sums.index_add_(0, owner, tab[s.uniq_id_d.long()])
+    assert torch.all(sums == M)
+    # the table has no duplicates and row 0 is the zero sentinel
+    assert torch.all(tab[0] == 0)
+    assert torch.unique(s.table_keys_d).numel() == s.table_keys_d.numel()
+    # uniq lists are strictly increasing within each anchor
+    ux = s.uniq_x_d.long()
+    inner = torch.ones_like(ux, dtype=torch.bool)
+    inner[s.offsets_d[:-1][s.anchor_counts() > 0]] = False
+    assert torch.all((ux[1:] > ux[:-1])[inner[1:]])
+
+
+def test_chi_square_transitions(wj):
+    """Each step is uniform over the current node's neighbours."""
+    from scipy.stats import chisquare
+
+    g = _er(2_000, 8_000, 11)
+    s = wj.preprocess(g, 200, 4, 17)
+    w = s.walks
+    for c in (5, 17, 123):
+        deg = g.degree(c)
+        if deg < 3:
+            continue
+        prev, nxt = w[:, :, :-1].reshape(-1), w[:, :, 1:].reshape(-1)
+        sel = nxt[prev == c]
+        counts = np.array([(sel == v).sum() for v in g.neighbors(c)])
+        assert counts.sum() == sel.size
+        assert chisquare(counts).pvalue > 1e-4
+
+
+def test_train_step_graph_matches_eager(wj):
+    """The captured training step equals the eager step (same RNG stream)."""
+    g = _er(3_000, 30_000, 2)
+    s = wj.preprocess(g, 50, 3, 5)
+    rng = np.random.default_rng(0)
+    q = torch.from_numpy(np.stack([rng.choice(3000, 2, replace=False) for _ in range(96)])).cuda()
+    y = torch.from_numpy((np.arange(96) < 8).astype(np.float32)).cuda()
+    outs = []
+    for use_graph in (False, True):
+        p = wj.init_params(2, 3, dropout=0.0, seed=1)
+        st = wj.AdamState.for_params(p)
+        step = wj.TrainStep(s, p, st, use_graph=use_graph)
+        losses = [float(step(q, y)) for _ in range(3)]
+        outs.append((losses, {k: v.clone() for k, v in p.tensors.items()}))
+    np.testing.assert_allclose(outs[0][0], outs[1][0], rtol=1e-6)
+    for k in outs[0][1]:
+        torch.testing.assert_close(outs[0][1][k], outs[1][1][k], rtol=1e-5, atol=1e-7)
