@@ -43,6 +43,7 @@ def lib():
         L.wjo_sample_node_walks.argtypes = [P, P, I64, I64, I64, U64, P]
         L.wjo_sample_node_walks.restype = U64
         L.wjo_sample_all_walks.argtypes = [P, P, I64, I64, I64, U64, P, I]
+        L.wjo_sample_nodes.argtypes = [P, P, P, I64, I64, I64, U64, P, I]
         L.wjo_count_distinct_all.argtypes = [P, I64, I64, I64, P, I]
         L.wjo_fill_distinct_all.argtypes = [P, I64, I64, I64, P, I64, P, P, I]
         L.wjo_intern_rows.argtypes = [P, I64, I64, P, P]
@@ -84,24 +85,71 @@ def sample_walks(idxptr, indices, u, num_walks, num_steps, state):
     return out, int(end)
 
 
-def sample_all_walks(idxptr, indices, num_walks, num_steps, seed, threads=None, lo=0, hi=None):
-    """_kernels.py:69-74 over nodes [lo, hi)."""
+def sample_all_walks(idxptr, indices, num_walks, num_steps, seed, threads=None):
+    """_kernels.py:69-74 over all nodes."""
     idxptr = np.ascontiguousarray(idxptr, np.int64)
     indices = np.ascontiguousarray(indices, np.int32)
     n = idxptr.shape[0] - 1
-    hi = n if hi is None else hi
-    walks = np.empty((hi - lo, num_walks, num_steps + 1), np.int32)
-    if hi > lo:
-        # shift the node range by calling per-node (keeps the C entry simple)
-        if lo == 0 and hi == n:
-            lib().wjo_sample_all_walks(_p(idxptr), _p(indices), n, num_walks, num_steps,
-                                       int(seed) & _MASK64, _p(walks), threads or default_threads())
-        else:
-            for k, u in enumerate(range(lo, hi)):
-                w, _ = sample_walks(idxptr, indices, u, num_walks, num_steps,
-                                    node_stream_state(seed, u))
-                walks[k] = w
+    walks = np.empty((n, num_walks, num_steps + 1), np.int32)
+    lib().wjo_sample_all_walks(_p(idxptr), _p(indices), n, num_walks, num_steps,
+                               int(seed) & _MASK64, _p(walks), threads or default_threads())
     return walks
+
+
+def sample_nodes(idxptr, indices, nodes, num_walks, num_steps, seed, threads=None):
+    """_kernels.py:69-74 for an explicit anchor list (rows in list order)."""
+    idxptr = np.ascontiguousarray(idxptr, np.int64)
+    indices = np.ascontiguousarray(indices, np.int32)
+    nodes = np.ascontiguousarray(nodes, np.int64)
+    walks = np.empty((nodes.shape[0], num_walks, num_steps + 1), np.int32)
+    lib().wjo_sample_nodes(_p(idxptr), _p(indices), _p(nodes), nodes.shape[0], num_walks,
+                           num_steps, int(seed) & _MASK64, _p(walks), threads or default_threads())
+    return walks
+
+
+def store_from_walks(walks, seed=0, threads=None, timed=False):
+    """sampler.py:117-151 on a given walk table (rows = anchors in order):
+    distinct lists, interning, dicts.  Used to time preprocess on a shard and
+    to build a batch's sub-store for the CPU baseline."""
+    import time
+
+    threads = threads or default_threads()
+    L = lib()
+    walks = np.ascontiguousarray(walks, np.int32)
+    n, num_walks, width = walks.shape
+    t = {}
+    local_cap = 1
+    while local_cap < 2 * num_walks * width:
+        local_cap <<= 1
+    t0 = time.perf_counter()
+    counts = np.empty(n, np.int64)
+    L.wjo_count_distinct_all(_p(walks), n, num_walks * width, local_cap, _p(counts), threads)
+    item_offsets = np.zeros(n + 1, np.int64)
+    np.cumsum(counts, out=item_offsets[1:])
+    total = int(item_offsets[-1])
+    t["count"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    nodes_flat = np.empty(total, np.int32)
+    vecs = np.empty((total, width), np.int32)
+    L.wjo_fill_distinct_all(_p(walks), n, num_walks, width, _p(item_offsets), local_cap,
+                            _p(nodes_flat), _p(vecs), threads)
+    t["fill"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    rpe_ids, table = intern_vectors(vecs)
+    del vecs
+    t["intern"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    caps = dict_capacities(counts)
+    cap_offsets = np.zeros(n + 1, np.int64)
+    np.cumsum(caps, out=cap_offsets[1:])
+    dict_keys = np.full(int(cap_offsets[-1]), -1, np.int32)
+    dict_vals = np.zeros(int(cap_offsets[-1]), np.int32)
+    L.wjo_build_dicts(_p(nodes_flat), _p(rpe_ids), _p(item_offsets), _p(cap_offsets), n,
+                      _p(dict_keys), _p(dict_vals), threads)
+    t["dicts"] = time.perf_counter() - t0
+    return OracleStore(n, num_walks, width - 1, int(seed) & _MASK64, walks, table, cap_offsets,
+                       dict_keys, dict_vals, item_offsets, nodes_flat, rpe_ids,
+                       phase_seconds=t if timed else None)
 
 
 def compute_rpe(walks: np.ndarray) -> dict:

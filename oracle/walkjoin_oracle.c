@@ -82,6 +82,21 @@ void wjo_sample_all_walks(const int64_t *idxptr, const int32_t *indices, int64_t
     }
 }
 
+/* K:69-74 restricted to an explicit anchor list (bench.py samples the
+ * anchors of one batch, or a contiguous shard, with their own streams). */
+void wjo_sample_nodes(const int64_t *idxptr, const int32_t *indices, const int64_t *nodes,
+                      int64_t count, int64_t num_walks, int64_t num_steps, uint64_t seed,
+                      int32_t *walks, int threads) {
+    set_threads(threads);
+    const int64_t block = num_walks * (num_steps + 1);
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int64_t k = 0; k < count; ++k) {
+        const int64_t u = nodes[k];
+        wjo_sample_node_walks(idxptr, indices, u, num_walks, num_steps,
+                              wjo_node_stream_state(seed, u), walks + k * block);
+    }
+}
+
 /* K:77-84 linear probe in a local table */
 static inline int64_t probe_local(const int64_t *keys, int64_t x, int64_t cap_mask) {
     int64_t h = (int64_t)(mix64((uint64_t)x) & (uint64_t)cap_mask);

@@ -205,9 +205,11 @@ class TrainStep:
     captured as one CUDA graph per batch shape (``use_graph``)."""
 
     def __init__(self, store: SubgraphStore, params: E.ModelParams, state: E.AdamState,
-                 dense_dtype=torch.float32, mode: str = "pooled", use_graph: bool = True):
+                 dense_dtype=torch.float32, mode: str = "pooled", use_graph: bool = True,
+                 process_group=None):
         self.store, self.params, self.state = store, params, state
         self.dense_dtype, self.mode, self.use_graph = dense_dtype, mode, use_graph
+        self.group = process_group
         self.dev = store.device
         self.inv_bc = torch.ones(2, dtype=params.w1.dtype, device=self.dev)
         self._host_bc = torch.ones(2, dtype=params.w1.dtype).pin_memory()
@@ -218,6 +220,10 @@ class TrainStep:
         logits, cache = E.forward(self.params, dense, training=True, mode=self.mode)
         loss = E.bce_loss(logits, y)
         grads = E.backward(self.params, cache, y)
+        if self.group is not None:
+            from .distributed import all_reduce_grads
+
+            all_reduce_grads(grads, E.TENSOR_ORDER, self.group)
         E.adam_step_graphable(self.params, grads, self.state, inv_bc)
         return loss
 

@@ -137,9 +137,29 @@ def intern_device(uniq_key, uniq_first, offsets, n_anchors, anchor_base, num_wal
     return uniq_id, table_keys
 
 
+class _Phases:
+    """Optional CUDA-event bracketing of preprocess phases (for bench.py)."""
+
+    def __init__(self, sink):
+        self.sink = sink
+        self.last = None
+
+    def mark(self, name):
+        if self.sink is None:
+            return
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        if self.last is not None:
+            self.sink.append((self.last[0], self.last[1], ev))
+        self.last = (name, ev)
+
+
 def preprocess(g, num_walks: int, num_steps: int, seed: int, threads: int = 1,
-               device=None, keep_keys: bool = False) -> SubgraphStore:
-    """Build the device store (Alg. 1, reference sampler.py:94-151)."""
+               device=None, keep_keys: bool = False, phases: list = None) -> SubgraphStore:
+    """Build the device store (Alg. 1, reference sampler.py:94-151).
+
+    ``phases`` (optional list) receives (name, start_event, end_event) per
+    phase: sample, rpe_count, rpe_fill, intern."""
     if num_walks < 1 or num_steps < 1:
         raise ValueError("num_walks and num_steps must be >= 1")
     if threads < 1:
@@ -154,10 +174,13 @@ def preprocess(g, num_walks: int, num_steps: int, seed: int, threads: int = 1,
     s = _lib.stream_handle(dev)
     walks = torch.empty((n, M, W), dtype=torch.int32, device=dev)
     flags = torch.zeros(n, dtype=torch.uint8, device=dev)
+    ph = _Phases(phases)
+    ph.mark("sample")
     _lib.call("wj_sample_walks", _lib.ptr(dg.idxptr), dg.idxptr_bytes, _lib.ptr(dg.indices), n, 0, n,
               M, L, seed64, _lib.ptr(walks), _lib.ptr(flags), s)
     del flags
     counts = torch.empty(n, dtype=torch.int32, device=dev)
+    ph.mark("rpe_count")
     _lib.call("wj_rpe_count", _lib.ptr(walks), n, M, L, n, _lib.ptr(counts), s)
     offsets = torch.zeros(n + 1, dtype=torch.int64, device=dev)
     torch.cumsum(counts, 0, out=offsets[1:])
@@ -167,9 +190,12 @@ def preprocess(g, num_walks: int, num_steps: int, seed: int, threads: int = 1,
     ukey = torch.empty(total, dtype=torch.int64, device=dev)
     ufirst = torch.empty(total, dtype=torch.int16, device=dev)
     slot = torch.empty((n, M * W), dtype=torch.int16, device=dev)
+    ph.mark("rpe_fill")
     _lib.call("wj_rpe_fill", _lib.ptr(walks), n, M, L, n, _lib.ptr(offsets), _lib.ptr(ux),
               _lib.ptr(ukey), _lib.ptr(ufirst), _lib.ptr(slot), s)
+    ph.mark("intern")
     uid, table_keys = intern_device(ukey, ufirst, offsets, n, 0, M, W)
+    ph.mark("end")
     store = SubgraphStore(n, M, L, seed64, walks, offsets, ux, uid, ufirst, slot, table_keys,
                           max_unique, id_map=getattr(g, "id_map", None))
     if keep_keys:
