@@ -109,6 +109,26 @@ int wj_join(const int64_t *queries, int64_t n_batch, int32_t arity, const int32_
             int32_t *rpe_ids_out, void *dense_out, int32_t dense_dtype, int64_t row_stride,
             wj_stream_t stream);
 
+/* Join fused with the encoder's first layer.  For every query b computes,
+ * without materialising the [A*M*(L+1), A*(L+1)] input or its [rows, H]
+ * hidden activations,
+ *   pooled_out[b, h] = sum_r relu(z_r[h]) * d_r[h]
+ *   s_out[b, c, h]   = sum_r x_r[c] * 1[z_r[h] > 0] * d_r[h]   (may be NULL)
+ *   msum_out[b, h]   = sum_r 1[z_r[h] > 0] * d_r[h]           (may be NULL)
+ * with z_r = x_r W1 + b1 (w1 [A*(L+1), hidden] fp32, row-major), x_r the
+ * joined RPE row of walk slot r and d_r a Bernoulli(keep_prob) dropout draw
+ * from a counter-based stream keyed by (seed, *step, b, anchor, slot, unit)
+ * (keep_prob = 1: no dropout).  *step is read on the device so a captured
+ * CUDA graph advances it itself.  Replaces _kernels.join_fill +
+ * pipeline._dense_batch + the first layer of encoder.forward/backward
+ * (_kernels.py:209-245, pipeline.py:169-182, encoder.py:150-161,224-232). */
+int wj_join_encode(const int64_t *queries, int64_t n_batch, int32_t arity, const int64_t *offsets,
+                   const int32_t *uniq_x, const int32_t *uniq_id, int32_t num_walks,
+                   int32_t num_steps, int32_t max_unique, const uint64_t *table_keys,
+                   int64_t table_len, const float *w1, const float *b1, int32_t hidden,
+                   float keep_prob, uint64_t seed, const int64_t *step, float *pooled_out,
+                   float *s_out, float *msum_out, wj_stream_t stream);
+
 /* Densify ids: out[i, :] = table[rpe_ids[i], :] (table [T, width] int32).
  * Replaces joiner.gather_rpe (joiner.py:96-104); *bad_flag set if an id is
  * out of range (the reference raises ValueError). */

@@ -32,6 +32,8 @@ SIGNATURES = {
     "wj_intern_insert": [P, P, P, I64, I64, P, P, I64, P, P],
     "wj_intern_assign": [P, I64, P, P, I64, P, P],
     "wj_join": [P, I64, I32, P, P, P, P, P, I32, I32, I32, P, I64, P, P, P, I32, I64, P],
+    "wj_join_encode": [P, I64, I32, P, P, P, I32, I32, I32, P, I64, P, P, I32, ctypes.c_float, U64,
+                       P, P, P, P, P],
     "wj_gather_rpe": [P, I64, P, I64, I32, P, I32, P, P],
     "wj_export_dicts": [P, P, P, P, P, I64, I32, I32, P, P, P, P],
     "wj_lookup": [P, P, I64, P, P, P, P, P],

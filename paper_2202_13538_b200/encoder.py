@@ -132,6 +132,54 @@ def forward(p: ModelParams, dense: torch.Tensor, training: bool = False,
     return logits, cache
 
 
+def forward_fused(p: ModelParams, store, q: torch.Tensor, training: bool = False, seed: int = 0,
+                  step: Optional[torch.Tensor] = None, need_grad: bool = True, out: dict = None):
+    """Encoder forward straight from query ids: the wj_join_encode kernel
+    joins, densifies and applies layer 1 (+ReLU, dropout, row mean and the
+    backward statistics) per query; the [B, 64]-sized rest runs in PyTorch.
+    Same math as ``forward`` (mode="pooled"); see csrc/encode.cu."""
+    from . import _lib
+
+    if p.feature_dim:
+        raise NotImplementedError("fused encoder takes RPE inputs only (use dense_batch + forward)")
+    if p.w1.dtype != torch.float32:
+        raise NotImplementedError("fused encoder computes in fp32")
+    B, A = q.shape
+    if A != p.arity:
+        raise ValueError(f"queries have arity {A} but model was trained with arity {p.arity}")
+    W = store.width
+    H, AW = p.hidden, A * W
+    dev = store.device
+    rows = A * store.landings
+    keep = (1.0 - p.dropout) if (training and p.dropout > 0.0) else 1.0
+    o = out if out is not None else {}
+    pooled = o.get("pooled")
+    if pooled is None:
+        pooled = torch.empty((B, H), dtype=torch.float32, device=dev)
+    S = msum = None
+    if need_grad:
+        S = o.get("S")
+        msum = o.get("msum")
+        if S is None:
+            S = torch.empty((B, AW, H), dtype=torch.float32, device=dev)
+            msum = torch.empty((B, H), dtype=torch.float32, device=dev)
+    t = p.tensors
+    _lib.call("wj_join_encode", _lib.ptr(q), B, A, _lib.ptr(store.offsets_d), _lib.ptr(store.uniq_x_d),
+              _lib.ptr(store.uniq_id_d), store.num_walks, store.walk_steps, store.max_unique,
+              _lib.ptr(store.table_keys_d), int(store.table_keys_d.numel()), _lib.ptr(t["w1"]),
+              _lib.ptr(t["b1"]), H, float(keep), int(seed) & ((1 << 64) - 1), _lib.ptr(step),
+              _lib.ptr(pooled), _lib.ptr(S), _lib.ptr(msum), _lib.stream_handle(dev))
+    pooled_mean = pooled / (keep * rows)
+    hq = torch.addmm(t["b2"], pooled_mean, t["w2"])
+    z2 = torch.addmm(t["c1"], hq, t["u1"])
+    relu2 = z2 > 0
+    a2 = torch.relu(z2)
+    logits = a2 @ t["u2"] + t["c2"][0]
+    cache = dict(pooled=pooled_mean, S=S, msum=msum, keep=keep, hq=hq, relu2=relu2, a2=a2,
+                 logits=logits, rows=rows, B=B, mode="fused", version=p.version)
+    return logits, cache
+
+
 def bce_loss(logits: torch.Tensor, labels: torch.Tensor) -> torch.Tensor:
     """Numerically stable mean BCE on the logit scale (encoder.py:183-188)."""
     z = logits
@@ -154,6 +202,12 @@ def backward(p: ModelParams, cache: dict, labels: torch.Tensor) -> dict:
     du1 = cache["hq"].t() @ dz2
     dhq = dz2 @ t["u1"].t()
     db2 = dhq.sum(0)
+    if cache["mode"] == "fused":
+        dw2 = cache["pooled"].t() @ dhq
+        g = (dhq @ t["w2"].t()) / (rows * cache["keep"])      # [B, h]
+        dw1 = torch.einsum("bch,bh->ch", cache["S"], g)
+        db1 = (cache["msum"] * g).sum(0)
+        return {"w1": dw1, "b1": db1, "w2": dw2, "b2": db2, "u1": du1, "c1": dc1, "u2": du2, "c2": dc2}
     if cache["mode"] == "reference":
         de = (dhq / rows).repeat_interleave(rows, dim=0)
         dw2 = cache["a1d"].t() @ de

@@ -201,23 +201,44 @@ def make_batch(index, positives: np.ndarray, pos_filter, cfg: TrainConfig, rng, 
 
 
 class TrainStep:
-    """join+densify -> forward -> BCE -> backward -> Adam on the device,
-    captured as one CUDA graph per batch shape (``use_graph``)."""
+    """One training step on the device, captured as a CUDA graph per batch
+    shape (``use_graph``).
+
+    mode="fused" (default): wj_join_encode (join + densify + layer 1 + ReLU +
+    dropout + row mean + backward statistics, one kernel) -> [B, 64] tail in
+    PyTorch -> BCE -> backward -> Adam.  mode="pooled" / "reference": the
+    wj_join dense kernel feeds the PyTorch encoder (``E.forward``)."""
 
     def __init__(self, store: SubgraphStore, params: E.ModelParams, state: E.AdamState,
-                 dense_dtype=torch.float32, mode: str = "pooled", use_graph: bool = True,
-                 process_group=None):
+                 dense_dtype=torch.float32, mode: str = "fused", use_graph: bool = True,
+                 process_group=None, seed: int = 0):
         self.store, self.params, self.state = store, params, state
         self.dense_dtype, self.mode, self.use_graph = dense_dtype, mode, use_graph
         self.group = process_group
+        self.seed = int(seed)
         self.dev = store.device
         self.inv_bc = torch.ones(2, dtype=params.w1.dtype, device=self.dev)
         self._host_bc = torch.ones(2, dtype=params.w1.dtype).pin_memory()
+        self.step_t = torch.zeros(1, dtype=torch.int64, device=self.dev)
         self._graphs: dict = {}
 
-    def _body(self, q, y, dense, inv_bc):
-        dense_batch(self.store, q, dtype=self.dense_dtype, out=dense, validate=False)
-        logits, cache = E.forward(self.params, dense, training=True, mode=self.mode)
+    def _buffers(self, B, A):
+        if self.mode == "fused":
+            H, AW = self.params.hidden, A * self.store.width
+            return {"pooled": torch.empty((B, H), device=self.dev),
+                    "S": torch.empty((B, AW, H), device=self.dev),
+                    "msum": torch.empty((B, H), device=self.dev)}
+        return {"dense": torch.empty((B, A * self.store.landings, A * self.store.width),
+                                     dtype=self.dense_dtype, device=self.dev)}
+
+    def _body(self, q, y, bufs, inv_bc):
+        self.step_t.add_(1)
+        if self.mode == "fused":
+            logits, cache = E.forward_fused(self.params, self.store, q, training=True, seed=self.seed,
+                                            step=self.step_t, out=bufs)
+        else:
+            dense_batch(self.store, q, dtype=self.dense_dtype, out=bufs["dense"], validate=False)
+            logits, cache = E.forward(self.params, bufs["dense"], training=True, mode=self.mode)
         loss = E.bce_loss(logits, y)
         grads = E.backward(self.params, cache, y)
         if self.group is not None:
@@ -235,13 +256,13 @@ class TrainStep:
         self.inv_bc.copy_(self._host_bc, non_blocking=True)
 
     def __call__(self, q: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
-        """q: [B, A] int64 device ids, y: [B] labels (device).  Returns the loss (device)."""
+        """q: [B, A] int64 ids, y: [B] labels (device, or pinned host for the
+        end-to-end path).  Returns the loss (device scalar)."""
         B, A = q.shape
         self._prepare_bc()
         if not self.use_graph:
-            dense = torch.empty((B, A * self.store.landings, A * self.store.width),
-                                dtype=self.dense_dtype, device=self.dev)
-            out = self._body(q, y.to(self.params.w1.dtype), dense, self.inv_bc)
+            out = self._body(q.to(self.dev, non_blocking=True), y.to(self.dev, self.params.w1.dtype),
+                             self._buffers(B, A), self.inv_bc)
             self.params.version += 1
             return out
         key = (B, A)
@@ -260,27 +281,28 @@ class TrainStep:
         q = torch.zeros((B, A), dtype=torch.int64, device=dev)
         q[:, :] = torch.arange(A, device=dev)[None, :] % max(self.store.num_nodes, 1)
         y = torch.zeros(B, dtype=self.params.w1.dtype, device=dev)
-        dense = torch.empty((B, A * self.store.landings, A * self.store.width), dtype=self.dense_dtype,
-                            device=dev)
+        bufs = self._buffers(B, A)
         # warm up on a side stream (allocator + cuBLAS handles), then capture;
-        # params / Adam state are snapshotted so warm-up leaves no trace
+        # params / Adam state / step counter are snapshotted so warm-up leaves no trace
         snap_p = {k: v.clone() for k, v in self.params.tensors.items()}
         snap_m = {k: v.clone() for k, v in self.state.m.items()}
         snap_v = {k: v.clone() for k, v in self.state.v.items()}
+        snap_step = self.step_t.clone()
         s = torch.cuda.Stream(dev)
         s.wait_stream(torch.cuda.current_stream(dev))
         with torch.cuda.stream(s):
             for _ in range(2):
-                self._body(q, y, dense, self.inv_bc)
+                self._body(q, y, bufs, self.inv_bc)
         torch.cuda.current_stream(dev).wait_stream(s)
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
-            loss = self._body(q, y, dense, self.inv_bc)
+            loss = self._body(q, y, bufs, self.inv_bc)
         for k in snap_p:
             self.params.tensors[k].copy_(snap_p[k])
             self.state.m[k].copy_(snap_m[k])
             self.state.v[k].copy_(snap_v[k])
-        return {"graph": graph, "q": q, "y": y, "dense": dense, "loss": loss}
+        self.step_t.copy_(snap_step)
+        return {"graph": graph, "q": q, "y": y, "bufs": bufs, "loss": loss}
 
 
 def infer(store: SubgraphStore, params: E.ModelParams, queries, threads: int = 1, features=None,
@@ -294,8 +316,12 @@ def infer(store: SubgraphStore, params: E.ModelParams, queries, threads: int = 1
     out = []
     q_all = torch.from_numpy(rows).to(store.device)
     for lo in range(0, rows.shape[0], chunk):
-        dense = dense_batch(store, q_all[lo: lo + chunk], features=features,
-                            dtype=params.w1.dtype)
-        logits, _ = E.forward(params, dense, training=False)
+        if features is None and params.feature_dim == 0 and params.w1.dtype == torch.float32:
+            logits, _ = E.forward_fused(params, store, q_all[lo: lo + chunk], training=False,
+                                        need_grad=False)
+        else:
+            dense = dense_batch(store, q_all[lo: lo + chunk], features=features,
+                                dtype=params.w1.dtype)
+            logits, _ = E.forward(params, dense, training=False)
         out.append(torch.sigmoid(logits.double()))
     return torch.cat(out).cpu().numpy()

@@ -252,9 +252,149 @@ def test_train_step_graph_matches_eager(wj):
     for use_graph in (False, True):
         p = wj.init_params(2, 3, dropout=0.0, seed=1)
         st = wj.AdamState.for_params(p)
-        step = wj.TrainStep(s, p, st, use_graph=use_graph)
+        step = wj.TrainStep(s, p, st, use_graph=use_graph, mode="pooled")
         losses = [float(step(q, y)) for _ in range(3)]
         outs.append((losses, {k: v.clone() for k, v in p.tensors.items()}))
     np.testing.assert_allclose(outs[0][0], outs[1][0], rtol=1e-6)
     for k in outs[0][1]:
         torch.testing.assert_close(outs[0][1][k], outs[1][1][k], rtol=1e-5, atol=1e-7)
+
+
+# ------------------------------------------------------------ fused encoder --
+
+_M64 = (1 << 64) - 1
+
+
+def _mix64(z):
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def _fused_model(store, q, w1, b1, keep, seed, step, warps=8):
+    """Host model of wj_join_encode: pooled / S / msum per query, including
+    the kernel's dropout stream (same counters, same row segmentation)."""
+    G = 0x9E3779B97F4A7C15
+    off = store.offsets_d.cpu().numpy()
+    ux = store.uniq_x_d.cpu().numpy()
+    uid = store.uniq_id_d.cpu().numpy()
+    T = store.table.vectors.astype(np.int64)
+    B, A = q.shape
+    W = store.width
+    P = store.landings
+    H = w1.shape[1]
+    thr = 65536 if keep >= 1 else int(keep * 65536.0 + 0.5)
+    skey = _mix64((seed + G * (step + 1)) & _M64)
+    pooled = np.zeros((B, H))
+    S = np.zeros((B, A * W, H))
+    msum = np.zeros((B, H))
+    for b in range(B):
+        lists = [(ux[off[q[b, j]]:off[q[b, j] + 1]], uid[off[q[b, j]]:off[q[b, j] + 1]]) for j in range(A)]
+        for a in range(A):
+            xa, ida = lists[a]
+            ids = np.zeros((len(xa), A), np.int64)
+            for j in range(A):
+                if j == a:
+                    ids[:, j] = ida
+                else:
+                    xj, idj = lists[j]
+                    pos = np.searchsorted(xj, xa)
+                    pos_c = np.minimum(pos, len(xj) - 1)
+                    ids[:, j] = np.where((pos < len(xj)) & (xj[pos_c] == xa), idj[pos_c], 0)
+            X = T[ids].reshape(len(xa), A * W).astype(np.float64)
+            n_l = T[ida].sum(1)
+            rowoff = np.concatenate([[0], np.cumsum(n_l)])
+            z = (b1[None, :].astype(np.float64) + X @ w1.astype(np.float64)).astype(np.float32)
+            kept = np.zeros((len(xa), H))
+            if thr >= 65536:
+                kept[:] = n_l[:, None]
+            else:
+                qkey = _mix64(skey ^ _mix64((b << 3) | a))
+                HU = H // 32
+                for w in range(warps):
+                    r, r_end = P * w // warps, P * (w + 1) // warps
+                    if r >= r_end:
+                        continue
+                    l = int(np.searchsorted(rowoff, r, side="right")) - 1
+                    while r < r_end:
+                        cnt = int(min(int(rowoff[l + 1]), r_end) - r)
+                        step_rows = max(4 // HU, 1)
+                        for t in range(0, cnt, step_rows):
+                            for lane in range(32):
+                                ctr = (((r + t) << 5) | lane) & _M64
+                                rnd = _mix64((qkey + ctr * G) & _M64)
+                                for s in range(4):
+                                    row, u = s // HU, s % HU
+                                    if t + row < cnt and ((rnd >> (16 * s)) & 0xFFFF) < thr:
+                                        kept[l, u * 32 + lane] += 1
+                        r += cnt
+                        l += 1
+            posm = z > 0
+            pooled[b] += (np.where(posm, z, 0) * kept).sum(0)
+            gk = posm * kept
+            msum[b] += gk.sum(0)
+            S[b] += X.T @ gk
+    return pooled, S, msum
+
+
+@pytest.mark.parametrize("keep", [1.0, 0.9])
+def test_fused_join_encode_matches_host_model(wj, keep):
+    g = _er(800, 6_000, 4)
+    s = wj.preprocess(g, 40, 4, 21)
+    rng = np.random.default_rng(3)
+    q = np.stack([rng.choice(800, 2, replace=False) for _ in range(12)]).astype(np.int64)
+    p = wj.init_params(2, 4, dropout=1 - keep, seed=2)
+    step = torch.tensor([6], dtype=torch.int64, device="cuda")
+    pooled = torch.empty((12, 64), device="cuda")
+    S = torch.empty((12, 10, 64), device="cuda")
+    msum = torch.empty((12, 64), device="cuda")
+    wj.encoder.forward_fused(p, s, torch.from_numpy(q).cuda(), training=keep < 1, seed=99, step=step,
+                             out={"pooled": pooled, "S": S, "msum": msum})
+    w1 = p.w1.cpu().numpy()
+    b1 = p.b1.cpu().numpy()
+    mp, mS, mm = _fused_model(s, q, w1, b1, keep, 99, 6)
+    np.testing.assert_allclose(pooled.cpu().numpy(), mp, rtol=2e-5, atol=1e-3)
+    assert np.mean(np.abs(S.cpu().numpy() - mS) < 0.5) > 0.999
+    assert np.mean(np.abs(msum.cpu().numpy() - mm) < 0.5) > 0.999
+    if keep < 1:  # kept fraction ~ keep
+        nod = _fused_model(s, q, w1, b1, 1.0, 99, 6)[2]
+        frac = mm.sum() / nod.sum()
+        assert abs(frac - keep) < 0.01
+
+
+@pytest.mark.parametrize("name", [c for c in golden_cases() if "logits" in load_golden(c)])
+def test_fused_logits_and_grads_vs_reference(wj, name):
+    """Fused path (no dropout) reproduces the reference logits and gradients."""
+    g = load_golden(name)
+    A, L = g["queries"].shape[1], int(g["L"])
+    store = wj.preprocess(_graph(wj, g), int(g["M"]), L, int(g["seed"]))
+    p = wj.encoder.params_from_numpy({k: g["p_" + k] for k in wj.encoder.TENSOR_ORDER}, A, L)
+    qd = torch.from_numpy(g["queries"]).cuda()
+    logits, cache = wj.encoder.forward_fused(p, store, qd, training=False)
+    ref = g["logits"]
+    np.testing.assert_allclose(logits.double().cpu().numpy(), ref, rtol=1e-5,
+                               atol=1e-5 * max(np.abs(ref).max(), 1e-3))
+    grads = wj.backward(p, cache, torch.from_numpy(g["labels"]).cuda())
+    for k in wj.encoder.TENSOR_ORDER:
+        r = g["g_" + k]
+        np.testing.assert_allclose(grads[k].double().cpu().numpy(), r, rtol=1e-4,
+                                   atol=1e-4 * max(np.abs(r).max(), 1e-12))
+
+
+def test_fused_train_step_graph(wj):
+    """Captured fused step == eager fused step; dropout masks change per step."""
+    g = _er(3_000, 30_000, 2)
+    s = wj.preprocess(g, 50, 3, 5)
+    rng = np.random.default_rng(0)
+    q = torch.from_numpy(np.stack([rng.choice(3000, 2, replace=False) for _ in range(96)])).cuda()
+    y = torch.from_numpy((np.arange(96) < 8).astype(np.float32)).cuda()
+    runs = []
+    for use_graph in (False, True):
+        p = wj.init_params(2, 3, dropout=0.1, seed=1)
+        st = wj.AdamState.for_params(p)
+        step = wj.TrainStep(s, p, st, use_graph=use_graph, mode="fused", seed=4)
+        losses = [float(step(q, y)) for _ in range(4)]
+        runs.append((losses, {k: v.clone() for k, v in p.tensors.items()}))
+    np.testing.assert_allclose(runs[0][0], runs[1][0], rtol=1e-5)
+    for k in runs[0][1]:
+        torch.testing.assert_close(runs[0][1][k], runs[1][1][k], rtol=1e-4, atol=1e-6)
