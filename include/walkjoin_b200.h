@@ -129,6 +129,25 @@ int wj_join_encode(const int64_t *queries, int64_t n_batch, int32_t arity, const
                    float keep_prob, uint64_t seed, const int64_t *step, float *pooled_out,
                    float *s_out, float *msum_out, wj_stream_t stream);
 
+/* Encoder tail on the wj_join_encode outputs (hidden = 64): W2 layer on the
+ * pooled encodings (pm = pooled * scale), 2-layer classifier, BCE and the
+ * full backward.  params is the flat fp32 parameter vector laid out by
+ * offsets9 = {w1, b1, w2, b2, u1, c1, u2, c2, total}.  Training (labels !=
+ * NULL) launches exactly partial_rows CTAs; CTA i writes its partial
+ * gradients to partial[i, 0:total] and its loss partial to partial[i, total].
+ * logits_out (may be NULL) gets the [B] logits.  Replaces encoder.forward /
+ * bce_loss / backward after layer 1 (encoder.py:159-233). */
+int wj_encoder_tail(const float *pooled, const float *s, const float *msum, const float *labels,
+                    int64_t n_batch, int32_t aw, int32_t hidden, const float *params,
+                    const int32_t *offsets9, float scale, float *logits_out, float *partial,
+                    int32_t partial_rows, wj_stream_t stream);
+
+/* Deterministic reduction of the partial gradients + bias-corrected Adam
+ * with t = *step (encoder.py:236-249).  grad_out / loss_out may be NULL. */
+int wj_adam(float *params, float *m, float *v, const float *partial, int32_t partial_rows,
+            int32_t n_params, float lr, float beta1, float beta2, float eps, const int64_t *step,
+            float *grad_out, float *loss_out, wj_stream_t stream);
+
 /* Densify ids: out[i, :] = table[rpe_ids[i], :] (table [T, width] int32).
  * Replaces joiner.gather_rpe (joiner.py:96-104); *bad_flag set if an id is
  * out of range (the reference raises ValueError). */

@@ -34,6 +34,9 @@ SIGNATURES = {
     "wj_join": [P, I64, I32, P, P, P, P, P, I32, I32, I32, P, I64, P, P, P, I32, I64, P],
     "wj_join_encode": [P, I64, I32, P, P, P, I32, I32, I32, P, I64, P, P, I32, ctypes.c_float, U64,
                        P, P, P, P, P],
+    "wj_encoder_tail": [P, P, P, P, I64, I32, I32, P, P, ctypes.c_float, P, P, I32, P],
+    "wj_adam": [P, P, P, P, I32, I32, ctypes.c_float, ctypes.c_float, ctypes.c_float, ctypes.c_float,
+                P, P, P, P],
     "wj_gather_rpe": [P, I64, P, I64, I32, P, I32, P, P],
     "wj_export_dicts": [P, P, P, P, P, I64, I32, I32, P, P, P, P],
     "wj_lookup": [P, P, I64, P, P, P, P, P],
@@ -77,6 +80,10 @@ def ptr(t) -> int | None:
     if t is None:
         return None
     return t.data_ptr()
+
+
+def sm_count_of(device) -> int:
+    return torch.cuda.get_device_properties(device).multi_processor_count
 
 
 def stream_handle(device=None) -> int:

@@ -78,6 +78,18 @@ def init_params(arity, walk_steps, hidden=64, feature_dim=0, dropout=0.1, seed=0
                        {k: torch.tensor(v, dtype=dtype, device=device) for k, v in host.items()})
 
 
+def flatten_params(p: ModelParams) -> tuple:
+    """Move the parameters into one flat fp32 buffer (TENSOR_ORDER) and make
+    ``p.tensors`` views of it.  Returns (flat, host int32 offsets
+    [w1, b1, w2, b2, u1, c1, u2, c2, total]) for the tail / Adam kernels."""
+    sizes = [p.tensors[k].numel() for k in TENSOR_ORDER]
+    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
+    flat = torch.cat([p.tensors[k].reshape(-1).to(torch.float32) for k in TENSOR_ORDER])
+    for k, o, n in zip(TENSOR_ORDER, offs[:-1], sizes):
+        p.tensors[k] = flat[o: o + n].view(p.tensors[k].shape)
+    return flat, offs
+
+
 def params_from_numpy(arrays: dict, arity, walk_steps, dropout=0.0, device="cuda",
                       dtype=torch.float32) -> ModelParams:
     t = {k: torch.tensor(np.asarray(arrays[k]), dtype=dtype, device=device) for k in TENSOR_ORDER}
@@ -133,7 +145,8 @@ def forward(p: ModelParams, dense: torch.Tensor, training: bool = False,
 
 
 def forward_fused(p: ModelParams, store, q: torch.Tensor, training: bool = False, seed: int = 0,
-                  step: Optional[torch.Tensor] = None, need_grad: bool = True, out: dict = None):
+                  step: Optional[torch.Tensor] = None, need_grad: bool = True, out: dict = None,
+                  tail: bool = True):
     """Encoder forward straight from query ids: the wj_join_encode kernel
     joins, densifies and applies layer 1 (+ReLU, dropout, row mean and the
     backward statistics) per query; the [B, 64]-sized rest runs in PyTorch.
@@ -169,6 +182,8 @@ def forward_fused(p: ModelParams, store, q: torch.Tensor, training: bool = False
               _lib.ptr(store.table_keys_d), int(store.table_keys_d.numel()), _lib.ptr(t["w1"]),
               _lib.ptr(t["b1"]), H, float(keep), int(seed) & ((1 << 64) - 1), _lib.ptr(step),
               _lib.ptr(pooled), _lib.ptr(S), _lib.ptr(msum), _lib.stream_handle(dev))
+    if not tail:
+        return None, None
     pooled_mean = pooled / (keep * rows)
     hq = torch.addmm(t["b2"], pooled_mean, t["w2"])
     z2 = torch.addmm(t["c1"], hq, t["u1"])

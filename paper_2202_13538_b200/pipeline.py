@@ -9,6 +9,7 @@ step is one graph launch plus the H2D copy of the batch's query ids.
 
 from __future__ import annotations
 
+import ctypes
 import logging
 import time
 from collections import deque
@@ -211,7 +212,7 @@ class TrainStep:
 
     def __init__(self, store: SubgraphStore, params: E.ModelParams, state: E.AdamState,
                  dense_dtype=torch.float32, mode: str = "fused", use_graph: bool = True,
-                 process_group=None, seed: int = 0):
+                 process_group=None, seed: int = 0, fast_tail: Optional[bool] = None):
         self.store, self.params, self.state = store, params, state
         self.dense_dtype, self.mode, self.use_graph = dense_dtype, mode, use_graph
         self.group = process_group
@@ -221,9 +222,35 @@ class TrainStep:
         self._host_bc = torch.ones(2, dtype=params.w1.dtype).pin_memory()
         self.step_t = torch.zeros(1, dtype=torch.int64, device=self.dev)
         self._graphs: dict = {}
+        # fused + hidden 64: tail and Adam as two CUDA kernels on flat buffers
+        self.fast_tail = (mode == "fused" and params.hidden == 64 and params.feature_dim == 0
+                          and params.w1.dtype == torch.float32 and process_group is None
+                          and store.width * params.arity in (2, 3, 4, 5, 6, 8, 9, 10, 12, 14, 15, 16))
+        if fast_tail is not None:
+            self.fast_tail = self.fast_tail and fast_tail
+        if self.fast_tail:
+            self.flat, self.offs = E.flatten_params(params)
+            self.m_flat = torch.cat([state.m[k].reshape(-1) for k in E.TENSOR_ORDER])
+            self.v_flat = torch.cat([state.v[k].reshape(-1) for k in E.TENSOR_ORDER])
+            for k, o, o2 in zip(E.TENSOR_ORDER, self.offs[:-1], self.offs[1:]):
+                state.m[k] = self.m_flat[o:o2].view(params.tensors[k].shape)
+                state.v[k] = self.v_flat[o:o2].view(params.tensors[k].shape)
+            self.offs_c = (ctypes.c_int32 * 9)(*[int(x) for x in self.offs])
+            from ._lib import sm_count_of
+
+            self.tail_rows = sm_count_of(self.dev)
+            self.loss_buf = torch.zeros(1, dtype=torch.float32, device=self.dev)
 
     def _buffers(self, B, A):
         if self.mode == "fused":
+            if self.fast_tail:
+                groups = (B + 7) // 8
+                rows = max(1, min(groups, self.tail_rows))
+                H, AW = self.params.hidden, A * self.store.width
+                return {"pooled": torch.empty((B, H), device=self.dev),
+                        "S": torch.empty((B, AW, H), device=self.dev),
+                        "msum": torch.empty((B, H), device=self.dev),
+                        "partial": torch.empty((rows, int(self.offs[-1]) + 1), device=self.dev)}
             H, AW = self.params.hidden, A * self.store.width
             return {"pooled": torch.empty((B, H), device=self.dev),
                     "S": torch.empty((B, AW, H), device=self.dev),
@@ -231,7 +258,30 @@ class TrainStep:
         return {"dense": torch.empty((B, A * self.store.landings, A * self.store.width),
                                      dtype=self.dense_dtype, device=self.dev)}
 
+    def _fast_body(self, q, y, bufs):
+        """fused kernel -> encoder tail kernel -> Adam kernel (3 launches)."""
+        from . import _lib
+
+        p, st, store = self.params, self.state, self.store
+        B, A = q.shape
+        self.step_t.add_(1)
+        E.forward_fused(p, store, q, training=True, seed=self.seed, step=self.step_t, out=bufs,
+                        tail=False)
+        keep = (1.0 - p.dropout) if p.dropout > 0.0 else 1.0
+        scale = 1.0 / (keep * A * store.landings)
+        dev = _lib.stream_handle(self.dev)
+        rows = bufs["partial"].shape[0]
+        _lib.call("wj_encoder_tail", _lib.ptr(bufs["pooled"]), _lib.ptr(bufs["S"]), _lib.ptr(bufs["msum"]),
+                  _lib.ptr(y), B, A * store.width, p.hidden, _lib.ptr(self.flat), self.offs_c, scale,
+                  None, _lib.ptr(bufs["partial"]), rows, dev)
+        _lib.call("wj_adam", _lib.ptr(self.flat), _lib.ptr(self.m_flat), _lib.ptr(self.v_flat),
+                  _lib.ptr(bufs["partial"]), rows, int(self.offs[-1]), st.lr, st.beta1, st.beta2,
+                  st.eps, _lib.ptr(self.step_t), None, _lib.ptr(self.loss_buf), dev)
+        return self.loss_buf[0]
+
     def _body(self, q, y, bufs, inv_bc):
+        if self.fast_tail:
+            return self._fast_body(q, y, bufs)
         self.step_t.add_(1)
         if self.mode == "fused":
             logits, cache = E.forward_fused(self.params, self.store, q, training=True, seed=self.seed,

@@ -398,3 +398,25 @@ def test_fused_train_step_graph(wj):
     np.testing.assert_allclose(runs[0][0], runs[1][0], rtol=1e-5)
     for k in runs[0][1]:
         torch.testing.assert_close(runs[0][1][k], runs[1][1][k], rtol=1e-4, atol=1e-6)
+
+
+def test_fast_tail_matches_torch_tail(wj):
+    """wj_encoder_tail + wj_adam (flat buffers, deterministic partial sums)
+    == the PyTorch tail of the same fused step, dropout included."""
+    g = _er(2_000, 20_000, 6)
+    s = wj.preprocess(g, 60, 4, 8)
+    rng = np.random.default_rng(1)
+    q = torch.from_numpy(np.stack([rng.choice(2000, 2, replace=False) for _ in range(203)])).cuda()
+    y = torch.from_numpy((np.arange(203) % 7 == 0).astype(np.float32)).cuda()
+    out = []
+    for fast in (False, True):
+        p = wj.init_params(2, 4, dropout=0.1, seed=3)
+        st = wj.AdamState.for_params(p)
+        step = wj.TrainStep(s, p, st, mode="fused", seed=9, use_graph=fast, fast_tail=fast)
+        assert step.fast_tail == fast
+        losses = [float(step(q, y)) for _ in range(3)]
+        out.append((losses, {k: v.clone() for k, v in p.tensors.items()}, {k: v.clone() for k, v in st.m.items()}))
+    np.testing.assert_allclose(out[0][0], out[1][0], rtol=2e-5)
+    for k in out[0][1]:
+        torch.testing.assert_close(out[0][1][k], out[1][1][k], rtol=1e-4, atol=2e-6)
+        torch.testing.assert_close(out[0][2][k], out[1][2][k], rtol=2e-3, atol=1e-7)
