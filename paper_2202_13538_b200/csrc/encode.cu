@@ -78,31 +78,47 @@ __device__ __forceinline__ int lb_s(const int32_t *a, int n, int32_t x) {
 }
 
 // A query anchors, AW = A * (L+1) input columns, HU = hidden units per lane
+//
+// Per query (one CTA, 8 warps) and per anchor block a:
+//  1. pre-pass, one thread per distinct landing l: its RPE ids against every
+//     query anchor, the non-zero entries of x_l (u16: c << 12 | count), the
+//     row count n_l, and a CTA-wide exclusive scan of (n_l, nnz_l);
+//  2. the block's P virtual rows are split evenly over the warps; a warp
+//     walks the landings of its row range: z = b1 + x W1 over the non-zero
+//     entries, kept counts from the dropout stream (one splitmix64 word per
+//     (row group, lane) covers 4/HU rows x HU units), then pooled / msum in
+//     registers and S in the warp's shared-memory accumulator.
 template <int A, int AW, int HU>
 __global__ void __launch_bounds__(kEncWarps * 32) join_encode_kernel(EncArgs g) {
     constexpr int H = HU * 32;
-    constexpr int NV = 2 + AW;  // accumulators per hidden unit: pooled, msum, S[AW]
+    constexpr int NV = 2 + AW;  // per-warp accumulators: pooled, msum, S[AW]
+    constexpr int RPW = 4 / HU > 0 ? 4 / HU : 1;  // rows per random word
+    constexpr int NT = kEncWarps * 32;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int W = g.W, P = g.P, mu = g.max_u;
+    const int P = g.P, mu = g.max_u;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float *w1s = reinterpret_cast<float *>(smem_raw);     // [AW][H]
     float *b1s = w1s + AW * H;                             // [H]
-    float *red = b1s + H;                                  // [warps][NV][H]
-    int64_t *qa = reinterpret_cast<int64_t *>(red + kEncWarps * NV * H);  // [4]
+    float *sacc = b1s + H;                                 // [warps][NV][H]
+    int64_t *qa = reinterpret_cast<int64_t *>(sacc + kEncWarps * NV * H);  // [4]
     int *un = reinterpret_cast<int *>(qa + 4);             // [4]
-    int32_t *sx = reinterpret_cast<int32_t *>(un + 4);     // [A][mu]
+    unsigned long long *wsum = reinterpret_cast<unsigned long long *>(un + 4);  // [warps + 1]
+    int32_t *sx = reinterpret_cast<int32_t *>(wsum + kEncWarps + 2);  // [A][mu]
     int32_t *sid = sx + A * mu;                            // [A][mu]
     int32_t *cross = sid + A * mu;                         // [A][A-1][mu]
-    int *rowoff = reinterpret_cast<int *>(cross + A * (A - 1) * mu);  // [mu + 1]
+    int2 *loc = reinterpret_cast<int2 *>(cross + A * (A - 1) * mu + 2);  // [mu + 1] {rowoff, nzoff}
+    uint16_t *nz = reinterpret_cast<uint16_t *>(loc + mu + 1);            // [mu * AW]
     uint64_t *tks = reinterpret_cast<uint64_t *>(
-        (reinterpret_cast<uintptr_t>(rowoff + mu + 1) + 15) & ~uintptr_t(15));
+        (reinterpret_cast<uintptr_t>(nz + (size_t)mu * AW) + 15) & ~uintptr_t(15));
     const uint64_t cmask = (1ULL << g.cb) - 1;
     const uint64_t skey = mix64(g.seed + kGolden * ((uint64_t)(g.step ? *g.step : 0) + 1ULL));
+    const bool dropout = g.keep_thr < 65536u;
+    float *my = sacc + warp * NV * H;
 
-    for (int i = threadIdx.x; i < AW * H; i += blockDim.x) w1s[i] = g.w1[i];
-    for (int i = threadIdx.x; i < H; i += blockDim.x) b1s[i] = g.b1[i];
+    for (int i = threadIdx.x; i < AW * H; i += NT) w1s[i] = g.w1[i];
+    for (int i = threadIdx.x; i < H; i += NT) b1s[i] = g.b1[i];
     if (g.stage_table)
-        for (int64_t i = threadIdx.x; i < g.tlen; i += blockDim.x) tks[i] = g.tkeys[i];
+        for (int64_t i = threadIdx.x; i < g.tlen; i += NT) tks[i] = g.tkeys[i];
 
     for (int64_t b = blockIdx.x; b < g.n_batch; b += gridDim.x) {
         if (threadIdx.x < A) {
@@ -110,11 +126,12 @@ __global__ void __launch_bounds__(kEncWarps * 32) join_encode_kernel(EncArgs g) 
             qa[threadIdx.x] = q;
             un[threadIdx.x] = (int)(g.offsets[q + 1] - g.offsets[q]);
         }
+        for (int i = lane; i < NV * H; i += 32) my[i] = 0.f;
         __syncthreads();
 #pragma unroll
         for (int a = 0; a < A; ++a) {
             const int64_t lo = g.offsets[qa[a]];
-            for (int i = threadIdx.x; i < un[a]; i += blockDim.x) {
+            for (int i = threadIdx.x; i < un[a]; i += NT) {
                 sx[a * mu + i] = __ldg(g.ux + lo + i);
                 sid[a * mu + i] = __ldg(g.uid + lo + i);
             }
@@ -128,7 +145,7 @@ __global__ void __launch_bounds__(kEncWarps * 32) join_encode_kernel(EncArgs g) 
                 const int nj = un[j];
                 const int32_t *xj = sx + j * mu;
                 int32_t *dst = cross + (a * (A - 1) + jj) * mu;
-                for (int k = threadIdx.x; k < un[a]; k += blockDim.x) {
+                for (int k = threadIdx.x; k < un[a]; k += NT) {
                     const int32_t x = sx[a * mu + k];
                     const int pos = lb_s(xj, nj, x);
                     dst[k] = (pos < nj && xj[pos] == x) ? sid[j * mu + pos] : 0;
@@ -136,119 +153,164 @@ __global__ void __launch_bounds__(kEncWarps * 32) join_encode_kernel(EncArgs g) 
             }
         }
 
-        float acc[NV][HU];
+        float pooled[HU], msum[HU];
 #pragma unroll
-        for (int v = 0; v < NV; ++v)
-#pragma unroll
-            for (int u = 0; u < HU; ++u) acc[v][u] = 0.f;
+        for (int u = 0; u < HU; ++u) pooled[u] = msum[u] = 0.f;
 
         for (int a = 0; a < A; ++a) {
             const int U = un[a];
-            __syncthreads();  // cross ready / previous rowoff consumers done
-            // rows per distinct landing: n_x = row sum of x's count vector wrt a
-            if (warp == 0) {
-                int carry = 0;
-                for (int base = 0; base < U; base += 32) {
-                    const int l = base + lane;
-                    int nl = 0;
-                    if (l < U) {
-                        const int id = sid[a * mu + l];
-                        const uint64_t key = g.stage_table ? tks[id] : __ldg(g.tkeys + id);
-                        for (int c = 0; c < W; ++c) nl += (int)((key >> (g.cb * c)) & cmask);
-                    }
-                    int incl = nl;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const int t = __shfl_up_sync(kFull, incl, o);
-                        if (lane >= o) incl += t;
-                    }
-                    if (l < U) rowoff[l] = carry + incl - nl;
-                    carry += __shfl_sync(kFull, incl, 31);
-                }
-                if (lane == 0) rowoff[U] = carry;  // == P
-            }
-            __syncthreads();
-            // this warp's slice of the block's P virtual rows
-            const int r_beg = (int)((int64_t)P * warp / kEncWarps);
-            const int r_end = (int)((int64_t)P * (warp + 1) / kEncWarps);
-            if (r_beg >= r_end) continue;
-            int l = ub_int(rowoff, U + 1, r_beg) - 1;
-            int r = r_beg;
-            const uint64_t qkey = mix64(skey ^ mix64(((uint64_t)b << 3) | (uint64_t)a));
-            while (r < r_end) {
-                const int l_end = rowoff[l + 1];
-                const int cnt = (l_end < r_end ? l_end : r_end) - r;
-                // x of this landing: A packed count vectors
-                uint64_t keys[A];
+            __syncthreads();  // cross ready; previous block's loc/nz consumers done
+            // ---- pre-pass: thread t owns landings [t*per, (t+1)*per)
+            const int per = (U + NT - 1) / NT;
+            const int l0 = threadIdx.x * per;
+            const int l1 = min(l0 + per, U);
+            unsigned long long tot = 0;  // (nnz << 32) | rows
+            for (int l = l0; l < l1; ++l) {
+                int rows = 0, cntnz = 0;
 #pragma unroll
                 for (int j = 0; j < A; ++j) {
                     const int id = (j == a) ? sid[a * mu + l]
                                             : cross[(a * (A - 1) + (j < a ? j : j - 1)) * mu + l];
-                    keys[j] = g.stage_table ? tks[id] : __ldg(g.tkeys + id);
+                    const uint64_t key = g.stage_table ? tks[id] : __ldg(g.tkeys + id);
+#pragma unroll
+                    for (int c = 0; c < AW / A; ++c) {
+                        const uint32_t v = (uint32_t)((key >> (g.cb * c)) & cmask);
+                        cntnz += v != 0;
+                        if (j == a) rows += (int)v;
+                    }
                 }
-                float xv[AW];
+                tot += ((unsigned long long)cntnz << 32) | (unsigned)rows;
+            }
+            // CTA exclusive scan of the per-thread totals
+            unsigned long long incl = tot;
 #pragma unroll
-                for (int j = 0; j < A; ++j)
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long t = __shfl_up_sync(kFull, incl, o);
+                if (lane >= o) incl += t;
+            }
+            if (lane == 31) wsum[warp] = incl;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                unsigned long long run = 0;
+                for (int w = 0; w < kEncWarps; ++w) {
+                    const unsigned long long t = wsum[w];
+                    wsum[w] = run;
+                    run += t;
+                }
+                wsum[kEncWarps] = run;
+            }
+            __syncthreads();
+            unsigned long long pos = wsum[warp] + incl - tot;
+            for (int l = l0; l < l1; ++l) {
+                int rows = 0;
+                int e = (int)(pos >> 32);
+                loc[l] = make_int2((int)(unsigned)pos, e);
 #pragma unroll
-                    for (int c = 0; c < AW / A; ++c)
-                        xv[j * (AW / A) + c] = (float)(uint32_t)((keys[j] >> (g.cb * c)) & cmask);
+                for (int j = 0; j < A; ++j) {
+                    const int id = (j == a) ? sid[a * mu + l]
+                                            : cross[(a * (A - 1) + (j < a ? j : j - 1)) * mu + l];
+                    const uint64_t key = g.stage_table ? tks[id] : __ldg(g.tkeys + id);
+#pragma unroll
+                    for (int c = 0; c < AW / A; ++c) {
+                        const uint32_t v = (uint32_t)((key >> (g.cb * c)) & cmask);
+                        if (v) nz[e++] = (uint16_t)(((j * (AW / A) + c) << 12) | v);
+                        if (j == a) rows += (int)v;
+                    }
+                }
+                pos += ((unsigned long long)(e - (int)(pos >> 32)) << 32) + (unsigned)rows;
+            }
+            if (threadIdx.x == 0) {
+                const unsigned long long t = wsum[kEncWarps];
+                loc[U] = make_int2((int)(unsigned)t, (int)(t >> 32));
+            }
+            __syncthreads();
+            // ---- rows of this warp
+            const int r_beg = (int)((int64_t)P * warp / kEncWarps);
+            const int r_end = (int)((int64_t)P * (warp + 1) / kEncWarps);
+            if (r_beg >= r_end) continue;
+            int l;
+            {
+                int lo_ = 0, hi_ = U + 1;  // first l with loc[l].x > r_beg, minus one
+                while (lo_ < hi_) {
+                    const int mid = (lo_ + hi_) >> 1;
+                    if (loc[mid].x <= r_beg)
+                        lo_ = mid + 1;
+                    else
+                        hi_ = mid;
+                }
+                l = lo_ - 1;
+            }
+            int r = r_beg;
+            const uint64_t qkey = mix64(skey ^ mix64(((uint64_t)b << 3) | (uint64_t)a));
+            int2 cur = loc[l];
+            int64_t word_idx = -1;
+            uint64_t rnd = 0;
+            while (r < r_end) {
+                const int2 nxt = loc[l + 1];
+                const int cnt = min(nxt.x, r_end) - r;
                 float z[HU];
 #pragma unroll
                 for (int u = 0; u < HU; ++u) z[u] = b1s[u * 32 + lane];
+                for (int e = cur.y; e < nxt.y; ++e) {
+                    const uint32_t ent = nz[e];
+                    const float v = (float)(ent & 0xFFFu);
+                    const float *wrow = w1s + (ent >> 12) * H + lane;
 #pragma unroll
-                for (int c = 0; c < AW; ++c) {
-                    if (xv[c] != 0.f) {  // warp-uniform: x is the same for every lane
-#pragma unroll
-                        for (int u = 0; u < HU; ++u) z[u] = fmaf(xv[c], w1s[c * H + u * 32 + lane], z[u]);
-                    }
+                    for (int u = 0; u < HU; ++u) z[u] = fmaf(v, wrow[u * 32], z[u]);
                 }
-                // kept rows per hidden unit among this landing's cnt rows
                 float kept[HU];
-                if (g.keep_thr >= 65536u) {
+                if (!dropout) {
 #pragma unroll
                     for (int u = 0; u < HU; ++u) kept[u] = (float)cnt;
                 } else {
                     int kc[HU];
 #pragma unroll
                     for (int u = 0; u < HU; ++u) kc[u] = 0;
-                    // one splitmix64 draw = 4 x 16-bit uniforms: (row pair) x (2 units)
-                    for (int t = 0; t < cnt; t += 4 / HU > 0 ? 4 / HU : 1) {
-                        const uint64_t ctr = ((uint64_t)(r + t) << 5) | (uint64_t)lane;
-                        const uint64_t rnd = mix64(qkey + ctr * kGolden);
-#pragma unroll
-                        for (int s = 0; s < 4; ++s) {
-                            const int row = s / HU, u = s % HU;
-                            if (row < 4 / HU && t + row < cnt)
-                                kc[u] += ((uint32_t)(rnd >> (16 * s)) & 0xFFFFu) < g.keep_thr;
+                    for (int row = r; row < r + cnt; ++row) {
+                        const int64_t wi = row / RPW;
+                        if (wi != word_idx) {
+                            word_idx = wi;
+                            rnd = mix64(qkey + (((uint64_t)wi << 5) | (uint64_t)lane) * kGolden);
                         }
+                        const int s0 = (row - (int)wi * RPW) * HU;
+#pragma unroll
+                        for (int u = 0; u < HU; ++u)
+                            kc[u] += ((uint32_t)(rnd >> (16 * (s0 + u))) & 0xFFFFu) < g.keep_thr;
                     }
 #pragma unroll
                     for (int u = 0; u < HU; ++u) kept[u] = (float)kc[u];
                 }
+                float gk[HU];
 #pragma unroll
                 for (int u = 0; u < HU; ++u) {
-                    const bool pos = z[u] > 0.f;
-                    const float gk = pos ? kept[u] : 0.f;
-                    acc[0][u] = fmaf(pos ? z[u] : 0.f, kept[u], acc[0][u]);
-                    acc[1][u] += gk;
+                    const bool pz = z[u] > 0.f;
+                    gk[u] = pz ? kept[u] : 0.f;
+                    pooled[u] = fmaf(pz ? z[u] : 0.f, kept[u], pooled[u]);
+                    msum[u] += gk[u];
+                }
+                for (int e = cur.y; e < nxt.y; ++e) {
+                    const uint32_t ent = nz[e];
+                    const float v = (float)(ent & 0xFFFu);
+                    float *srow = my + (2 + (ent >> 12)) * H + lane;
 #pragma unroll
-                    for (int c = 0; c < AW; ++c)
-                        if (xv[c] != 0.f) acc[2 + c][u] = fmaf(xv[c], gk, acc[2 + c][u]);
+                    for (int u = 0; u < HU; ++u) srow[u * 32] = fmaf(v, gk[u], srow[u * 32]);
                 }
                 r += cnt;
                 ++l;
+                cur = nxt;
             }
         }
-        // CTA reduction of the per-warp partial sums, then one store per value
+        // ---- CTA reduction of the per-warp accumulators, one store per value
 #pragma unroll
-        for (int v = 0; v < NV; ++v)
-#pragma unroll
-            for (int u = 0; u < HU; ++u) red[(warp * NV + v) * H + u * 32 + lane] = acc[v][u];
+        for (int u = 0; u < HU; ++u) {
+            my[u * 32 + lane] = pooled[u];
+            my[H + u * 32 + lane] = msum[u];
+        }
         __syncthreads();
-        for (int i = threadIdx.x; i < NV * H; i += blockDim.x) {
+        for (int i = threadIdx.x; i < NV * H; i += NT) {
             float s = 0.f;
 #pragma unroll
-            for (int w = 0; w < kEncWarps; ++w) s += red[w * NV * H + i];
+            for (int w = 0; w < kEncWarps; ++w) s += sacc[w * NV * H + i];
             const int v = i / H, h = i - v * H;
             if (v == 0)
                 g.pooled[b * H + h] = s;
@@ -336,9 +398,9 @@ extern "C" int wj_join_encode(const int64_t *queries, int64_t n_batch, int32_t a
     g.s_out = s_out;
     g.msum = msum_out;
     const int AW = arity * W, H = hidden;
-    size_t base = (size_t)(AW * H + H + kEncWarps * (2 + AW) * H) * 4 + 64 +
-                  (size_t)arity * g.max_u * 8 + (size_t)arity * (arity - 1) * g.max_u * 4 +
-                  (size_t)(g.max_u + 1) * 4 + 16;
+    size_t base = (size_t)(AW * H + H + kEncWarps * (2 + AW) * H) * 4 + 64 + 8 * (kEncWarps + 2) +
+                  (size_t)arity * g.max_u * 8 + (size_t)arity * (arity - 1) * g.max_u * 4 + 8 +
+                  (size_t)(g.max_u + 1) * 8 + (size_t)g.max_u * AW * 2 + 32;
     const size_t limit = 200 * 1024;
     g.stage_table = (base + (size_t)table_len * 8 <= limit && table_len <= 8192) ? 1 : 0;
     const size_t smem = base + (g.stage_table ? (size_t)table_len * 8 : 0);

@@ -309,26 +309,21 @@ def _fused_model(store, q, w1, b1, keep, seed, step, warps=8):
             if thr >= 65536:
                 kept[:] = n_l[:, None]
             else:
+                # draw of (row, unit u, lane): word (row // RPW, lane), field (row % RPW) * HU + u
                 qkey = _mix64(skey ^ _mix64((b << 3) | a))
                 HU = H // 32
-                for w in range(warps):
-                    r, r_end = P * w // warps, P * (w + 1) // warps
-                    if r >= r_end:
-                        continue
-                    l = int(np.searchsorted(rowoff, r, side="right")) - 1
-                    while r < r_end:
-                        cnt = int(min(int(rowoff[l + 1]), r_end) - r)
-                        step_rows = max(4 // HU, 1)
-                        for t in range(0, cnt, step_rows):
-                            for lane in range(32):
-                                ctr = (((r + t) << 5) | lane) & _M64
-                                rnd = _mix64((qkey + ctr * G) & _M64)
-                                for s in range(4):
-                                    row, u = s // HU, s % HU
-                                    if t + row < cnt and ((rnd >> (16 * s)) & 0xFFFF) < thr:
-                                        kept[l, u * 32 + lane] += 1
-                        r += cnt
-                        l += 1
+                rpw = max(4 // HU, 1)
+                owner = np.repeat(np.arange(len(xa)), n_l)  # local of each virtual row
+                for wi in range((P + rpw - 1) // rpw):
+                    for lane in range(32):
+                        rnd = _mix64((qkey + ((wi << 5) | lane) * G) & _M64)
+                        for rr in range(rpw):
+                            row = wi * rpw + rr
+                            if row >= P:
+                                break
+                            for u in range(HU):
+                                if ((rnd >> (16 * (rr * HU + u))) & 0xFFFF) < thr:
+                                    kept[owner[row], u * 32 + lane] += 1
             posm = z > 0
             pooled[b] += (np.where(posm, z, 0) * kept).sum(0)
             gk = posm * kept
