@@ -1,0 +1,79 @@
+"""Host-side product logic on CPU: graph ingestion, query validation,
+mini-batcher and negative sampler (exact reference draws), dict capacities."""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+
+def test_graph_from_edges_matches_reference_csr():
+    import paper_2202_13538_b200 as wj
+
+    for name in ("er300", "sparse400", "sbm2x100", "hyper60_a3"):
+        g = load_golden(name)
+        n = int(g["n"])
+        src = np.repeat(np.arange(n), np.diff(g["idxptr"]))
+        pairs = np.stack([src, g["indices"]], 1)
+        mine = wj.Graph.from_edges(pairs, n)
+        np.testing.assert_array_equal(mine.idxptr, g["idxptr"])
+        np.testing.assert_array_equal(mine.indices, g["indices"])
+    p = wj.load_edge_list(["0 1"])
+    assert p.idxptr.tolist() == [0, 1, 2] and p.indices.tolist() == [1, 0]
+    with pytest.raises(wj.GraphFormatError):
+        wj.load_edge_list(["0 1 2"])
+    with pytest.raises(wj.GraphFormatError):
+        wj.load_edge_list([])
+    with pytest.raises(ValueError):
+        wj.Query((1, 1))
+    with pytest.raises(ValueError):
+        wj.Query((1, 2), label=3)
+
+
+def test_dict_capacities_matches_oracle():
+    from oracle import core
+    from paper_2202_13538_b200.store import dict_capacities
+
+    c = np.array([0, 1, 2, 3, 4, 5, 63, 64, 65, 528, 1000])
+    np.testing.assert_array_equal(dict_capacities(c), core.dict_capacities(c))
+
+
+def test_minibatcher_and_negatives_reproduce_reference(golden_meta):
+    from paper_2202_13538_b200.pipeline import (PositiveFilter, QueryOverlapIndex, TrainConfig,
+                                                sample_minibatch, sample_negatives)
+
+    mb = golden_meta["minibatch"]
+    pos = np.asarray(mb["train_pos"], np.int64)
+    index = QueryOverlapIndex(pos)
+    allpos = np.concatenate([pos, np.asarray(mb["pos_filter_extra"], np.int64)])
+    n = int(allpos.max()) + 1
+    filt = PositiveFilter(allpos, n)
+    cfg = TrainConfig(batch_capacity=mb["batch_capacity"], batch_size=mb["batch_size"], k_neg=mb["k_neg"])
+    rng = np.random.default_rng(mb["rng_seed"])
+    for want in mb["batches"]:
+        seeds, ids = sample_minibatch(index, pos, cfg, rng, exact=True)
+        negs = sample_negatives(seeds, 2, cfg.k_neg * len(ids), filt, rng)
+        assert seeds == want["seeds"] and ids == want["ids"]
+        assert negs.tolist() == want["negs"]
+    # the fast seed draw gives a valid batch of the same shape contract
+    seeds, ids = sample_minibatch(index, pos, cfg, np.random.default_rng(0))
+    assert 0 < len(ids) <= cfg.batch_size and len(seeds) <= cfg.batch_capacity
+    assert all(any(v in set(seeds) for v in pos[i]) for i in ids)
+
+
+def test_train_config_validation():
+    from paper_2202_13538_b200.pipeline import TrainConfig
+
+    with pytest.raises(ValueError):
+        TrainConfig(k_neg=0)
+    with pytest.raises(ValueError):
+        TrainConfig(metric="f1")
+
+
+def test_product_does_not_import_oracle():
+    import pathlib
+
+    root = pathlib.Path(__file__).resolve().parents[1] / "paper_2202_13538_b200"
+    for f in root.rglob("*.py"):
+        src = f.read_text()
+        assert "import oracle" not in src and "from oracle" not in src, f
