@@ -13,7 +13,9 @@ from .sampler import RawRpeMap, WalkRng, WalkSet, compute_rpe, preprocess, sampl
 from .store import NodeEntry, RpeTable, StoreFormatError, SubgraphStore, dict_capacities, get_rpe_id
 from .joiner import JoinedQuery, dense_batch, gather_rpe, join_batch, join_batch_arrays, join_query
 from .encoder import AdamState, ModelParams, adam_step, backward, bce_loss, forward, init_params
-from .pipeline import TrainConfig, TrainStep, infer
+from .pipeline import QuerySplit, TrainConfig, TrainStep, infer, score_array, train, validation_metric
+from .metrics import RankedQueryResult, hits_at_k, mrr, rank_of_positive, roc_auc
+from .seeds import derive_seed
 
 _dense_batch = dense_batch  # reference call-site name (pipeline.py:169)
 
@@ -25,5 +27,6 @@ __all__ = [
     "RpeTable", "NodeEntry", "SubgraphStore", "StoreFormatError", "dict_capacities", "get_rpe_id",
     "JoinedQuery", "join_query", "join_batch", "join_batch_arrays", "gather_rpe", "dense_batch",
     "ModelParams", "AdamState", "init_params", "forward", "backward", "bce_loss", "adam_step",
-    "TrainConfig", "TrainStep", "infer",
+    "TrainConfig", "TrainStep", "QuerySplit", "train", "infer", "score_array", "validation_metric",
+    "RankedQueryResult", "rank_of_positive", "mrr", "hits_at_k", "roc_auc", "derive_seed",
 ]

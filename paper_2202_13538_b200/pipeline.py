@@ -13,7 +13,7 @@ import ctypes
 import logging
 import time
 from collections import deque
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
 import numpy as np
@@ -212,8 +212,12 @@ class TrainStep:
 
     def __init__(self, store: SubgraphStore, params: E.ModelParams, state: E.AdamState,
                  dense_dtype=torch.float32, mode: str = "fused", use_graph: bool = True,
-                 process_group=None, seed: int = 0, fast_tail: Optional[bool] = None):
+                 process_group=None, seed: int = 0, fast_tail: Optional[bool] = None,
+                 features: Optional[torch.Tensor] = None):
+        if features is not None and mode == "fused":
+            raise ValueError("node features need mode='pooled' or 'reference' (the fused kernel is RPE-only)")
         self.store, self.params, self.state = store, params, state
+        self.features = features
         self.dense_dtype, self.mode, self.use_graph = dense_dtype, mode, use_graph
         self.group = process_group
         self.seed = int(seed)
@@ -255,7 +259,8 @@ class TrainStep:
             return {"pooled": torch.empty((B, H), device=self.dev),
                     "S": torch.empty((B, AW, H), device=self.dev),
                     "msum": torch.empty((B, H), device=self.dev)}
-        return {"dense": torch.empty((B, A * self.store.landings, A * self.store.width),
+        d = 0 if self.features is None else int(self.features.shape[1])
+        return {"dense": torch.empty((B, A * self.store.landings, A * self.store.width + d),
                                      dtype=self.dense_dtype, device=self.dev)}
 
     def _fast_body(self, q, y, bufs):
@@ -287,7 +292,8 @@ class TrainStep:
             logits, cache = E.forward_fused(self.params, self.store, q, training=True, seed=self.seed,
                                             step=self.step_t, out=bufs)
         else:
-            dense_batch(self.store, q, dtype=self.dense_dtype, out=bufs["dense"], validate=False)
+            dense_batch(self.store, q, dtype=self.dense_dtype, out=bufs["dense"], validate=False,
+                        features=self.features)
             logits, cache = E.forward(self.params, bufs["dense"], training=True, mode=self.mode)
         loss = E.bce_loss(logits, y)
         grads = E.backward(self.params, cache, y)
@@ -353,6 +359,140 @@ class TrainStep:
             self.state.v[k].copy_(snap_v[k])
         self.step_t.copy_(snap_step)
         return {"graph": graph, "q": q, "y": y, "bufs": bufs, "loss": loss}
+
+
+@dataclass
+class QuerySplit:
+    """Inductive link-query split (graph.py:123-132): positives per phase,
+    per-positive negative groups for evaluation, and the walk graph with the
+    training edges removed.  Any object with these attributes (e.g. the
+    reference's own QuerySplit) is accepted by ``train``."""
+
+    train_pos: list
+    valid_pos: list
+    test_pos: list
+    valid_neg: list = field(default_factory=list)
+    test_neg: list = field(default_factory=list)
+    train_graph: object = None
+
+
+def _rows(queries) -> np.ndarray:
+    if isinstance(queries, np.ndarray):
+        return queries.astype(np.int64, copy=False)
+    if len(queries) == 0:
+        return np.empty((0, 0), np.int64)
+    return np.asarray([getattr(q, "nodes", q) for q in queries], dtype=np.int64)
+
+
+def score_array(store: SubgraphStore, params: E.ModelParams, query_array, features=None,
+                chunk: int = 8192) -> torch.Tensor:
+    """Sigmoid scores of a query array as a float64 DEVICE tensor
+    (pipeline.py:185-198 without the host round trip).  RPE-only fp32 models
+    score through the fused join+encode kernel; feature models through the
+    dense join kernel + PyTorch encoder."""
+    q_all = torch.as_tensor(query_array, dtype=torch.int64).to(store.device)
+    if q_all.shape[0] == 0:
+        return torch.empty(0, dtype=torch.float64, device=store.device)
+    out = []
+    for lo in range(0, q_all.shape[0], chunk):
+        q = q_all[lo: lo + chunk]
+        if features is None and params.feature_dim == 0 and params.w1.dtype == torch.float32:
+            logits, _ = E.forward_fused(params, store, q, training=False, need_grad=False)
+        else:
+            dense = dense_batch(store, q, features=features, dtype=params.w1.dtype, validate=False)
+            logits, _ = E.forward(params, dense, training=False)
+        out.append(torch.sigmoid(logits.double()))
+    return torch.cat(out)
+
+
+def validation_metric(store: SubgraphStore, params: E.ModelParams, split, cfg: TrainConfig,
+                      features=None, phase: str = "valid") -> float:
+    """pipeline.py:214-238 on the device: AUC over all positive / negative
+    scores, or MRR of each positive among its own negative group."""
+    from . import metrics as Mx
+
+    pos_q = _rows(getattr(split, f"{phase}_pos"))
+    groups = getattr(split, f"{phase}_neg")
+    flat = [getattr(q, "nodes", q) for grp in groups for q in grp]
+    if not flat:
+        raise ValueError(f"validation requires negative queries (split.{phase}_neg is empty)")
+    pos = score_array(store, params, pos_q, features)
+    neg = score_array(store, params, np.asarray(flat, dtype=np.int64), features)
+    if cfg.metric == "auc":
+        return Mx.roc_auc_device(pos, neg)
+    return Mx.mrr_device(pos, neg, [len(g) for g in groups[: pos_q.shape[0]]])
+
+
+def train(store: SubgraphStore, split, cfg: TrainConfig, features=None, train_negatives=None,
+          use_graph: bool = True, exact_batches: bool = False):
+    """Mini-batched training with early stopping (pipeline.py:241-326), same
+    seeds, batch contract and history; every step runs on the device
+    (``TrainStep``).  Returns (best params, history).
+
+    ``exact_batches=True`` draws the BFS seed nodes with the reference's
+    ``rng.choice`` (a permutation per batch), so with the same seed every
+    batch -- positives, negatives, labels -- is the reference's own; with
+    dropout off the trajectory then differs from the reference only by fp32
+    vs fp64 rounding."""
+    from .seeds import derive_seed
+
+    positives = _rows(split.train_pos)
+    if positives.shape[0] == 0:
+        raise ValueError("empty training set")
+    arity = positives.shape[1]
+    if not len(split.valid_pos):
+        raise ValueError("training requires validation positives for early stopping")
+    if cfg.use_features and features is None and getattr(split, "train_graph", None) is not None:
+        features = getattr(split.train_graph, "node_features", None)
+    features = features if cfg.use_features else None
+    if features is not None:
+        features = np.asarray(features, dtype=np.float64)
+        if features.shape[0] != store.num_nodes:
+            raise ValueError(f"feature matrix has {features.shape[0]} rows for {store.num_nodes} nodes")
+    feature_dim = 0 if features is None else int(features.shape[1])
+    dev = store.device
+    params = E.init_params(arity, store.walk_steps, hidden=cfg.hidden_dim, feature_dim=feature_dim,
+                           dropout=cfg.dropout, seed=derive_seed(cfg.seed, "init"), device=dev)
+    state = E.AdamState.for_params(params, lr=cfg.lr)
+    index = QueryOverlapIndex(positives)
+    filt_rows = [positives] + [_rows(g) for g in (split.valid_pos, split.test_pos) if len(g)]
+    pos_filter = PositiveFilter(np.concatenate(filt_rows), store.num_nodes)
+    batch_rng = np.random.default_rng(derive_seed(cfg.seed, "minibatch"))
+    pool = _rows(train_negatives) if train_negatives is not None and len(train_negatives) else None
+    feats_d = None if features is None else torch.as_tensor(features, dtype=torch.float32, device=dev)
+    step = TrainStep(store, params, state, mode="fused" if feats_d is None else "pooled",
+                     use_graph=use_graph, seed=derive_seed(cfg.seed, "dropout"), features=feats_d)
+    history = []
+    best_params, best_metric, best_epoch = params.copy(), -np.inf, 0
+    for epoch in range(1, cfg.max_epochs + 1):
+        t0 = time.perf_counter()
+        consumed, n_steps = 0, 0
+        loss_sum = torch.zeros((), dtype=torch.float64, device=dev)
+        while consumed < positives.shape[0]:
+            seeds, ids = sample_minibatch(index, positives, cfg, batch_rng, exact=exact_batches)
+            if not ids:
+                break
+            pos = positives[np.asarray(ids, dtype=np.int64)]
+            n_neg = cfg.k_neg * len(ids)
+            if pool is not None:
+                negs = pool[batch_rng.integers(0, pool.shape[0], size=n_neg)]
+            else:
+                negs = sample_negatives(seeds, arity, n_neg, pos_filter, batch_rng)
+            q = torch.from_numpy(np.concatenate([pos, negs]).astype(np.int64))
+            y = torch.from_numpy(np.concatenate([np.ones(len(ids)), np.zeros(negs.shape[0])]).astype(np.float32))
+            loss_sum += step(q, y).double()
+            consumed += len(ids)
+            n_steps += 1
+        valid = validation_metric(store, params, split, cfg, features=feats_d)
+        train_loss = float(loss_sum) / max(n_steps, 1)
+        history.append({"epoch": epoch, "train_loss": train_loss, "valid_metric": valid})
+        logger.info("epoch %d train_loss %.6f valid_%s %.6f wall %.2fs", epoch, train_loss, cfg.metric,
+                    valid, time.perf_counter() - t0)
+        if valid > best_metric:
+            best_metric, best_params, best_epoch = valid, params.copy(), epoch
+        if epoch - best_epoch >= cfg.patience:
+            break
+    return best_params, history
 
 
 def infer(store: SubgraphStore, params: E.ModelParams, queries, threads: int = 1, features=None,
