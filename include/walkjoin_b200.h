@@ -117,9 +117,11 @@ int wj_join(const int64_t *queries, int64_t n_batch, int32_t arity, const int32_
  *   msum_out[b, h]   = sum_r 1[z_r[h] > 0] * d_r[h]           (may be NULL)
  * with z_r = x_r W1 + b1 (w1 [A*(L+1), hidden] fp32, row-major), x_r the
  * joined RPE row of walk slot r and d_r a Bernoulli(keep_prob) dropout draw
- * from a counter-based stream keyed by (seed, *step, b, anchor, slot, unit)
+ * from a counter-based stream keyed by (seed, *step, b, landing, unit)
  * (keep_prob = 1: no dropout).  *step is read on the device so a captured
- * CUDA graph advances it itself.  Replaces _kernels.join_fill +
+ * CUDA graph advances it itself.  hidden = 64, A*(L+1) <= 15, M <= 2048 run
+ * the tensor-core kernel (encode_mma.cu); other shapes the SIMT kernel
+ * (wj_join_encode_simt).  Replaces _kernels.join_fill +
  * pipeline._dense_batch + the first layer of encoder.forward/backward
  * (_kernels.py:209-245, pipeline.py:169-182, encoder.py:150-161,224-232). */
 int wj_join_encode(const int64_t *queries, int64_t n_batch, int32_t arity, const int64_t *offsets,
@@ -128,6 +130,16 @@ int wj_join_encode(const int64_t *queries, int64_t n_batch, int32_t arity, const
                    int64_t table_len, const float *w1, const float *b1, int32_t hidden,
                    float keep_prob, uint64_t seed, const int64_t *step, float *pooled_out,
                    float *s_out, float *msum_out, wj_stream_t stream);
+
+/* Same contract on CUDA cores only (hidden in {32, 64, 128}, A*(L+1) <= 16);
+ * its dropout stream differs from wj_join_encode's tensor-core kernel. */
+int wj_join_encode_simt(const int64_t *queries, int64_t n_batch, int32_t arity,
+                        const int64_t *offsets, const int32_t *uniq_x, const int32_t *uniq_id,
+                        int32_t num_walks, int32_t num_steps, int32_t max_unique,
+                        const uint64_t *table_keys, int64_t table_len, const float *w1,
+                        const float *b1, int32_t hidden, float keep_prob, uint64_t seed,
+                        const int64_t *step, float *pooled_out, float *s_out, float *msum_out,
+                        wj_stream_t stream);
 
 /* Encoder tail on the wj_join_encode outputs (hidden = 64): W2 layer on the
  * pooled encodings (pm = pooled * scale), 2-layer classifier, BCE and the

@@ -349,7 +349,7 @@ static EncKernel pick(int A, int W, int hu) {
 
 }  // namespace wj
 
-extern "C" int wj_join_encode(const int64_t *queries, int64_t n_batch, int32_t arity,
+extern "C" int wj_join_encode_simt(const int64_t *queries, int64_t n_batch, int32_t arity,
                               const int64_t *offsets, const int32_t *uniq_x,
                               const int32_t *uniq_id, int32_t num_walks, int32_t num_steps,
                               int32_t max_unique, const uint64_t *table_keys, int64_t table_len,

@@ -43,6 +43,34 @@ struct TailArgs {
     float *partial;       // [grid, total + 1] (last column: loss partial)
 };
 
+// out[c] = sum_k in[k] M[k][c] for the lane's columns c = lane, lane + 32
+// (in: the warp's 64-vector, lane holds k = lane, lane + 32).  Four
+// independent accumulator chains per output instead of one 64-long chain.
+__device__ __forceinline__ void matvec(const float (&in)[2], const float *Ms, int lane, float (&out)[2]) {
+    float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+    for (int k = 0; k < kH; ++k) {
+        const float x = __shfl_sync(kFull, in[k >> 5], k & 31);
+        acc[0][k & 3] = fmaf(x, Ms[k * kPitch + lane], acc[0][k & 3]);
+        acc[1][k & 3] = fmaf(x, Ms[k * kPitch + lane + 32], acc[1][k & 3]);
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) out[j] = (acc[j][0] + acc[j][1]) + (acc[j][2] + acc[j][3]);
+}
+
+// out[r] = sum_h in[h] M[r][h] for the lane's rows r = lane, lane + 32
+__device__ __forceinline__ void matvec_t(const float (&in)[2], const float *Ms, int lane, float (&out)[2]) {
+    float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+    for (int h = 0; h < kH; ++h) {
+        const float x = __shfl_sync(kFull, in[h >> 5], h & 31);
+        acc[0][h & 3] = fmaf(x, Ms[lane * kPitch + h], acc[0][h & 3]);
+        acc[1][h & 3] = fmaf(x, Ms[(lane + 32) * kPitch + h], acc[1][h & 3]);
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) out[j] = (acc[j][0] + acc[j][1]) + (acc[j][2] + acc[j][3]);
+}
+
 template <int AW>
 __global__ void __launch_bounds__(kTailWarps * 32) encoder_tail_kernel(TailArgs g) {
     __shared__ float wts[2 * kH * kPitch];
@@ -83,19 +111,13 @@ __global__ void __launch_bounds__(kTailWarps * 32) encoder_tail_kernel(TailArgs 
         if (active) {
 #pragma unroll
             for (int j = 0; j < 2; ++j) pm[j] = g.pooled[b * kH + lane + 32 * j] * g.scale;
-            hq[0] = b2v[0];
-            hq[1] = b2v[1];
-            for (int k = 0; k < kH; ++k) {
-                const float pk = __shfl_sync(kFull, pm[k >> 5], k & 31);
-                hq[0] = fmaf(pk, w2s[k * kPitch + lane], hq[0]);
-                hq[1] = fmaf(pk, w2s[k * kPitch + lane + 32], hq[1]);
-            }
-            float z2[2] = {c1v[0], c1v[1]};
-            for (int k = 0; k < kH; ++k) {
-                const float hk = __shfl_sync(kFull, hq[k >> 5], k & 31);
-                z2[0] = fmaf(hk, u1s[k * kPitch + lane], z2[0]);
-                z2[1] = fmaf(hk, u1s[k * kPitch + lane + 32], z2[1]);
-            }
+            matvec(pm, w2s, lane, hq);  // hq = pm W2 + b2
+            hq[0] += b2v[0];
+            hq[1] += b2v[1];
+            float z2[2];
+            matvec(hq, u1s, lane, z2);  // z2 = hq U1 + c1
+            z2[0] += c1v[0];
+            z2[1] += c1v[1];
             const float a2[2] = {fmaxf(z2[0], 0.f), fmaxf(z2[1], 0.f)};
             float part = a2[0] * u2v[0] + a2[1] * u2v[1];
 #pragma unroll
@@ -115,20 +137,12 @@ __global__ void __launch_bounds__(kTailWarps * 32) encoder_tail_kernel(TailArgs 
                     dc1[j] += dz2[j];
                 }
                 // dhq[k] = sum_h dz2[h] U1[k][h], k = lane, lane + 32
-                for (int h = 0; h < kH; ++h) {
-                    const float dh = __shfl_sync(kFull, dz2[h >> 5], h & 31);
-                    dhq[0] = fmaf(dh, u1s[lane * kPitch + h], dhq[0]);
-                    dhq[1] = fmaf(dh, u1s[(lane + 32) * kPitch + h], dhq[1]);
-                }
+                matvec_t(dz2, u1s, lane, dhq);
                 db2[0] += dhq[0];
                 db2[1] += dhq[1];
                 // gk[k] = sum_h dhq[h] W2[k][h] * scale, k = lane, lane + 32
-                float gk[2] = {0.f, 0.f};
-                for (int h = 0; h < kH; ++h) {
-                    const float dh = __shfl_sync(kFull, dhq[h >> 5], h & 31);
-                    gk[0] = fmaf(dh, w2s[lane * kPitch + h], gk[0]);
-                    gk[1] = fmaf(dh, w2s[(lane + 32) * kPitch + h], gk[1]);
-                }
+                float gk[2];
+                matvec_t(dhq, w2s, lane, gk);
                 gk[0] *= g.scale;
                 gk[1] *= g.scale;
 #pragma unroll
@@ -244,26 +258,39 @@ __global__ void __launch_bounds__(kTailWarps * 32) encoder_tail_kernel(TailArgs 
 
 // Sum the per-CTA partial gradients in a fixed order and apply Adam
 // (encoder.py:236-249) with bias corrections from the device step counter.
-__global__ void adam_kernel(float *params, float *m, float *v, const float *partial, int rows,
-                            int n, float lr, float beta1, float beta2, float eps,
-                            const int64_t *step, float *grad_out, float *loss_out) {
+// A CTA owns 32 consecutive parameters; its 8 warps each sum every 8th
+// partial row (coalesced 128-B rows), then warp 0 adds the 8 sums in order:
+// deterministic, and 8x the memory parallelism of one thread per column.
+constexpr int kAdamCols = 32, kAdamGroups = 8;
+
+__global__ void __launch_bounds__(kAdamCols *kAdamGroups) adam_kernel(
+    float *params, float *m, float *v, const float *partial, int rows, int n, float lr, float beta1,
+    float beta2, float eps, const int64_t *step, float *grad_out, float *loss_out) {
+    __shared__ float part[kAdamGroups][kAdamCols];
+    const int c = threadIdx.x & (kAdamCols - 1), grp = threadIdx.x / kAdamCols;
+    const int i = blockIdx.x * kAdamCols + c;
+    float gsum = 0.f;
+    if (i <= n)
+        for (int r = grp; r < rows; r += kAdamGroups) gsum += partial[(int64_t)r * (n + 1) + i];
+    part[grp][c] = gsum;
+    __syncthreads();
+    if (grp != 0 || i > n) return;
+    gsum = 0.f;
+#pragma unroll
+    for (int k = 0; k < kAdamGroups; ++k) gsum += part[k][c];
+    if (i == n) {
+        if (loss_out) *loss_out = gsum;
+        return;
+    }
     const int64_t t = *step;
     const float bc1 = 1.f - powf(beta1, (float)t);
     const float bc2 = 1.f - powf(beta2, (float)t);
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += gridDim.x * blockDim.x) {
-        float gsum = 0.f;
-        for (int r = 0; r < rows; ++r) gsum += partial[(int64_t)r * (n + 1) + i];
-        if (i == n) {
-            if (loss_out) *loss_out = gsum;
-            continue;
-        }
-        if (grad_out) grad_out[i] = gsum;
-        const float mi = beta1 * m[i] + (1.f - beta1) * gsum;
-        const float vi = beta2 * v[i] + (1.f - beta2) * gsum * gsum;
-        m[i] = mi;
-        v[i] = vi;
-        params[i] -= lr * (mi / bc1) / (sqrtf(vi / bc2) + eps);
-    }
+    if (grad_out) grad_out[i] = gsum;
+    const float mi = beta1 * m[i] + (1.f - beta1) * gsum;
+    const float vi = beta2 * v[i] + (1.f - beta2) * gsum * gsum;
+    m[i] = mi;
+    v[i] = vi;
+    params[i] -= lr * (mi / bc1) / (sqrtf(vi / bc2) + eps);
 }
 
 using TailKernel = void (*)(TailArgs);
@@ -329,9 +356,8 @@ extern "C" int wj_adam(float *params, float *m, float *v, const float *partial,
         set_error("bad adam sizes");
         return WJ_ERR_ARG;
     }
-    const int threads = 256;
-    const int blocks = (n_params + 1 + threads - 1) / threads;
-    adam_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(
+    const int blocks = (n_params + 1 + kAdamCols - 1) / kAdamCols;
+    adam_kernel<<<blocks, kAdamCols * kAdamGroups, 0, (cudaStream_t)stream>>>(
         params, m, v, partial, partial_rows, n_params, lr, beta1, beta2, eps, step, grad_out, loss_out);
     return check_launch("wj_adam");
 }

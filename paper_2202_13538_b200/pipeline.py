@@ -242,7 +242,7 @@ class TrainStep:
             self.offs_c = (ctypes.c_int32 * 9)(*[int(x) for x in self.offs])
             from ._lib import sm_count_of
 
-            self.tail_rows = sm_count_of(self.dev)
+            self.tail_rows = 2 * sm_count_of(self.dev)
             self.loss_buf = torch.zeros(1, dtype=torch.float32, device=self.dev)
 
     def _buffers(self, B, A):

@@ -332,8 +332,93 @@ def _fused_model(store, q, w1, b1, keep, seed, step, warps=8):
     return pooled, S, msum
 
 
+_M32 = (1 << 32) - 1
+
+
+def _hash32(x):
+    x = np.asarray(x, dtype=np.uint64)
+    x ^= x >> np.uint64(16)
+    x = (x * np.uint64(0x7FEB352D)) & np.uint64(_M32)
+    x ^= x >> np.uint64(15)
+    x = (x * np.uint64(0x846CA68B)) & np.uint64(_M32)
+    x ^= x >> np.uint64(16)
+    return x
+
+
+def _binomial_thresholds(keep):
+    k = float(np.float32(keep))
+    if k >= 1.0:
+        return [(0, 0), (65536, 0), (65536, 65536)]
+    return [(0, 0), (int(k * 65536.0 + 0.5), 0),
+            (int((1.0 - (1.0 - k) * (1.0 - k)) * 65536.0 + 0.5), int(k * k * 65536.0 + 0.5))]
+
+
+def _fused_model_mma(store, q, w1, b1, keep, seed, step):
+    """Host model of the tensor-core wj_join_encode: virtual landings of <= 2
+    rows, Binomial(cnt, keep) kept rows by inverse CDF from the kernel's
+    hash32 stream; pooled / S / msum per query (float64)."""
+    G = 0x9E3779B97F4A7C15
+    off = store.offsets_d.cpu().numpy()
+    ux = store.uniq_x_d.cpu().numpy()
+    uid = store.uniq_id_d.cpu().numpy()
+    T = store.table.vectors.astype(np.int64)
+    B, A = q.shape
+    W = store.width
+    H = w1.shape[1]
+    thr = _binomial_thresholds(keep)
+    skey = _mix64((seed + G * (step + 1)) & _M64)
+    h = np.arange(H)
+    gq, mt, hb = h % 8, (h // 8) // 2, (h // 8) % 2
+    pooled = np.zeros((B, H))
+    S = np.zeros((B, A * W, H))
+    msum = np.zeros((B, H))
+    for b in range(B):
+        qlo = _mix64(skey ^ _mix64(b)) & _M32
+        lists = [(ux[off[q[b, j]]:off[q[b, j] + 1]], uid[off[q[b, j]]:off[q[b, j] + 1]]) for j in range(A)]
+        rows_x, cnts = [], []
+        for a in range(A):
+            xa, ida = lists[a]
+            ids = np.zeros((len(xa), A), np.int64)
+            for j in range(A):
+                if j == a:
+                    ids[:, j] = ida
+                else:
+                    xj, idj = lists[j]
+                    pos = np.searchsorted(xj, xa)
+                    pos_c = np.minimum(pos, len(xj) - 1)
+                    ids[:, j] = np.where((pos < len(xj)) & (xj[pos_c] == xa), idj[pos_c], 0)
+            X = T[ids].reshape(len(xa), A * W)
+            n_l = T[ida].sum(1)
+            for l in range(len(xa)):
+                r = int(n_l[l])
+                while r > 0:
+                    rows_x.append(X[l])
+                    cnts.append(min(r, 2))
+                    r -= 2
+        X = np.asarray(rows_x, np.float64)
+        cnt = np.asarray(cnts)
+        V = X.shape[0]
+        z = (b1[None, :].astype(np.float64) + X @ w1.astype(np.float64)).astype(np.float32)
+        v = np.arange(V, dtype=np.uint64)[:, None]
+        word = _hash32(np.uint64(qlo) ^ ((v << np.uint64(5)) | (gq[None, :].astype(np.uint64) << np.uint64(2))
+                                          | mt[None, :].astype(np.uint64)))
+        u = np.where(hb[None, :] == 1, word >> np.uint64(16), word & np.uint64(0xFFFF)).astype(np.int64)
+        t1 = np.array([thr[c][0] for c in cnt])[:, None]
+        t2 = np.array([thr[c][1] for c in cnt])[:, None]
+        kept = (u < t1).astype(np.float64) + (u < t2)
+        posm = z > 0
+        pooled[b] = (np.where(posm, z, 0) * kept).sum(0)
+        gk = posm * kept
+        msum[b] = gk.sum(0)
+        S[b] = X.T @ gk
+    return pooled, S, msum
+
+
 @pytest.mark.parametrize("keep", [1.0, 0.9])
-def test_fused_join_encode_matches_host_model(wj, keep):
+@pytest.mark.parametrize("kernel", ["mma", "simt"])
+def test_fused_join_encode_matches_host_model(wj, keep, kernel):
+    from paper_2202_13538_b200 import _lib
+
     g = _er(800, 6_000, 4)
     s = wj.preprocess(g, 40, 4, 21)
     rng = np.random.default_rng(3)
@@ -343,18 +428,62 @@ def test_fused_join_encode_matches_host_model(wj, keep):
     pooled = torch.empty((12, 64), device="cuda")
     S = torch.empty((12, 10, 64), device="cuda")
     msum = torch.empty((12, 64), device="cuda")
-    wj.encoder.forward_fused(p, s, torch.from_numpy(q).cuda(), training=keep < 1, seed=99, step=step,
-                             out={"pooled": pooled, "S": S, "msum": msum})
+    qd = torch.from_numpy(q).cuda()
+    _lib.call("wj_join_encode" if kernel == "mma" else "wj_join_encode_simt", _lib.ptr(qd), 12, 2,
+              _lib.ptr(s.offsets_d), _lib.ptr(s.uniq_x_d), _lib.ptr(s.uniq_id_d), s.num_walks, s.walk_steps,
+              s.max_unique, _lib.ptr(s.table_keys_d), int(s.table_keys_d.numel()), _lib.ptr(p.w1),
+              _lib.ptr(p.b1), 64, float(keep), 99, _lib.ptr(step), _lib.ptr(pooled), _lib.ptr(S),
+              _lib.ptr(msum), _lib.stream_handle(torch.device("cuda", 0)))
     w1 = p.w1.cpu().numpy()
     b1 = p.b1.cpu().numpy()
-    mp, mS, mm = _fused_model(s, q, w1, b1, keep, 99, 6)
+    model = _fused_model_mma if kernel == "mma" else _fused_model
+    mp, mS, mm = model(s, q, w1, b1, keep, 99, 6)
     np.testing.assert_allclose(pooled.cpu().numpy(), mp, rtol=2e-5, atol=1e-3)
+    # S and msum are integer-weighted sums: exact unless a z sits within rounding of 0
     assert np.mean(np.abs(S.cpu().numpy() - mS) < 0.5) > 0.999
     assert np.mean(np.abs(msum.cpu().numpy() - mm) < 0.5) > 0.999
     if keep < 1:  # kept fraction ~ keep
-        nod = _fused_model(s, q, w1, b1, 1.0, 99, 6)[2]
+        nod = model(s, q, w1, b1, 1.0, 99, 6)[2]
         frac = mm.sum() / nod.sum()
         assert abs(frac - keep) < 0.01
+
+
+def test_dropout_stream_statistics(wj):
+    """Kept-row counts of the tensor-core kernel: mean keep * rows, binomial
+    variance, and no correlation between neighbouring units / landings."""
+    from paper_2202_13538_b200 import _lib
+
+    g = _er(3_000, 40_000, 5)
+    s = wj.preprocess(g, 100, 4, 13)
+    rng = np.random.default_rng(8)
+    q = torch.from_numpy(np.stack([rng.choice(3000, 2, replace=False) for _ in range(256)])).cuda()
+    keep = 0.9
+    p = wj.init_params(2, 4, dropout=0.0, seed=4)
+    with torch.no_grad():  # z > 0 everywhere: msum counts kept rows
+        p.tensors["w1"].abs_()
+        p.tensors["b1"].fill_(0.5)
+    outs = []
+    for st in range(6):
+        step = torch.tensor([st], dtype=torch.int64, device="cuda")
+        ms = torch.empty((256, 64), device="cuda")
+        pooled = torch.empty((256, 64), device="cuda")
+        S = torch.empty((256, 10, 64), device="cuda")
+        _lib.call("wj_join_encode", _lib.ptr(q), 256, 2, _lib.ptr(s.offsets_d), _lib.ptr(s.uniq_x_d),
+                  _lib.ptr(s.uniq_id_d), s.num_walks, s.walk_steps, s.max_unique, _lib.ptr(s.table_keys_d),
+                  int(s.table_keys_d.numel()), _lib.ptr(p.w1), _lib.ptr(p.b1), 64, keep, 7, _lib.ptr(step),
+                  _lib.ptr(pooled), _lib.ptr(S), _lib.ptr(ms), _lib.stream_handle(torch.device("cuda", 0)))
+        outs.append(ms.double().cpu().numpy())
+    rows = 2 * s.landings
+    k = np.stack(outs)  # [steps, B, 64] kept rows out of `rows`
+    frac = k / rows
+    assert abs(frac.mean() - keep) < 2e-3
+    # each entry is a sum of `rows` Bernoulli(keep): var = rows * keep * (1 - keep)
+    var = k.var(axis=0).mean()
+    assert 0.8 < var / (rows * keep * (1 - keep)) < 1.25
+    # steps decorrelated, units decorrelated
+    c_steps = np.corrcoef(k[0].ravel(), k[1].ravel())[0, 1]
+    c_units = np.corrcoef(k[:, :, :-1].ravel(), k[:, :, 1:].ravel())[0, 1]
+    assert abs(c_steps) < 0.05 and abs(c_units) < 0.05
 
 
 @pytest.mark.parametrize("name", [c for c in golden_cases() if "logits" in load_golden(c)])
