@@ -160,6 +160,12 @@ int wj_adam(float *params, float *m, float *v, const float *partial, int32_t par
             int32_t n_params, float lr, float beta1, float beta2, float eps, const int64_t *step,
             float *grad_out, float *loss_out, wj_stream_t stream);
 
+/* Fixed-order column sums out[c] = sum_r partial[r, c] of a [rows, n_cols]
+ * partial buffer (the data-parallel step reduces locally, all-reduces the
+ * [n_params + 1] result over ranks, then runs wj_adam on it as one row). */
+int wj_sum_partials(const float *partial, int32_t partial_rows, int32_t n_cols, float *out,
+                    wj_stream_t stream);
+
 /* Densify ids: out[i, :] = table[rpe_ids[i], :] (table [T, width] int32).
  * Replaces joiner.gather_rpe (joiner.py:96-104); *bad_flag set if an id is
  * out of range (the reference raises ValueError). */

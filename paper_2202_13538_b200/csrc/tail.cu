@@ -293,6 +293,25 @@ __global__ void __launch_bounds__(kAdamCols *kAdamGroups) adam_kernel(
     params[i] -= lr * (mi / bc1) / (sqrtf(vi / bc2) + eps);
 }
 
+// Fixed-order column sums of the partial rows (the data-parallel path:
+// reduce locally, all-reduce the [n+1] vector over ranks, then Adam on it).
+__global__ void __launch_bounds__(kAdamCols *kAdamGroups) sum_rows_kernel(const float *partial, int rows,
+                                                                        int cols, float *out) {
+    __shared__ float part[kAdamGroups][kAdamCols];
+    const int c = threadIdx.x & (kAdamCols - 1), grp = threadIdx.x / kAdamCols;
+    const int i = blockIdx.x * kAdamCols + c;
+    float gsum = 0.f;
+    if (i < cols)
+        for (int r = grp; r < rows; r += kAdamGroups) gsum += partial[(int64_t)r * cols + i];
+    part[grp][c] = gsum;
+    __syncthreads();
+    if (grp != 0 || i >= cols) return;
+    gsum = 0.f;
+#pragma unroll
+    for (int k = 0; k < kAdamGroups; ++k) gsum += part[k][c];
+    out[i] = gsum;
+}
+
 using TailKernel = void (*)(TailArgs);
 
 static TailKernel pick_tail(int aw) {
@@ -360,4 +379,17 @@ extern "C" int wj_adam(float *params, float *m, float *v, const float *partial,
     adam_kernel<<<blocks, kAdamCols * kAdamGroups, 0, (cudaStream_t)stream>>>(
         params, m, v, partial, partial_rows, n_params, lr, beta1, beta2, eps, step, grad_out, loss_out);
     return check_launch("wj_adam");
+}
+
+extern "C" int wj_sum_partials(const float *partial, int32_t partial_rows, int32_t n_cols, float *out,
+                               wj_stream_t stream) {
+    using namespace wj;
+    if (n_cols < 1 || partial_rows < 1) {
+        set_error("bad partial sizes");
+        return WJ_ERR_ARG;
+    }
+    const int blocks = (n_cols + kAdamCols - 1) / kAdamCols;
+    sum_rows_kernel<<<blocks, kAdamCols * kAdamGroups, 0, (cudaStream_t)stream>>>(partial, partial_rows, n_cols,
+                                                                                 out);
+    return check_launch("wj_sum_partials");
 }

@@ -33,9 +33,21 @@ def shard_range(n: int, world: int, rank: int):
     return rank * n // world, (rank + 1) * n // world
 
 
+_NCCL_DTYPES = (torch.uint8, torch.int8, torch.int32, torch.int64, torch.float16, torch.bfloat16,
+                torch.float32, torch.float64)
+
+
 def all_gather_variable(t: torch.Tensor, group=None) -> list:
     """All-gather tensors whose first dimension differs per rank (pad to the
-    max, one all_gather_into_tensor, slice).  Works on gloo (CPU) and NCCL."""
+    max, one all_gather, slice).  Works on gloo (CPU) and NCCL; dtypes NCCL
+    lacks (int16 slot indices, uint16 first-appearance slots) travel as bytes."""
+    if t.dtype not in _NCCL_DTYPES:
+        dt = t.dtype
+        rows = t.shape[0]
+        per_row = t.element_size() * (t[0].numel() if rows else int(torch.tensor(t.shape[1:]).prod()))
+        as_bytes = t.contiguous().view(torch.uint8).reshape(rows, per_row)
+        return [p.reshape(-1).view(dt).reshape((p.shape[0],) + tuple(t.shape[1:]))
+                for p in all_gather_variable(as_bytes, group)]
     world = dist.get_world_size(group)
     n = torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device)
     sizes = [torch.zeros_like(n) for _ in range(world)]
@@ -124,12 +136,20 @@ def preprocess_sharded(g, num_walks: int, num_steps: int, seed: int, threads: in
                          int(counts.max().item()) if n else 0, id_map=getattr(g, "id_map", None))
 
 
+def all_reduce_mean(t: torch.Tensor, group=None) -> None:
+    """In-place mean over ranks: one ncclAllReduce(avg) on NCCL (capturable
+    in a CUDA graph), sum + divide on gloo."""
+    if dist.get_backend(group) == "nccl":
+        dist.all_reduce(t, op=dist.ReduceOp.AVG, group=group)
+    else:
+        dist.all_reduce(t, group=group)
+        t.div_(dist.get_world_size(group))
+
+
 def all_reduce_grads(grads: dict, order, group=None) -> None:
     """Average the encoder gradients over ranks with one flat all-reduce."""
-    world = dist.get_world_size(group)
     flat = torch.cat([grads[k].reshape(-1) for k in order])
-    dist.all_reduce(flat, group=group)
-    flat.div_(world)
+    all_reduce_mean(flat, group)
     off = 0
     for k in order:
         n = grads[k].numel()

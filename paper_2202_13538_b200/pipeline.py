@@ -228,7 +228,7 @@ class TrainStep:
         self._graphs: dict = {}
         # fused + hidden 64: tail and Adam as two CUDA kernels on flat buffers
         self.fast_tail = (mode == "fused" and params.hidden == 64 and params.feature_dim == 0
-                          and params.w1.dtype == torch.float32 and process_group is None
+                          and params.w1.dtype == torch.float32
                           and store.width * params.arity in (2, 3, 4, 5, 6, 8, 9, 10, 12, 14, 15, 16))
         if fast_tail is not None:
             self.fast_tail = self.fast_tail and fast_tail
@@ -244,6 +244,8 @@ class TrainStep:
 
             self.tail_rows = 2 * sm_count_of(self.dev)
             self.loss_buf = torch.zeros(1, dtype=torch.float32, device=self.dev)
+            if process_group is not None:  # data parallel: [grads | loss] all-reduced
+                self.grad_flat = torch.zeros(int(self.offs[-1]) + 1, dtype=torch.float32, device=self.dev)
 
     def _buffers(self, B, A):
         if self.mode == "fused":
@@ -279,8 +281,16 @@ class TrainStep:
         _lib.call("wj_encoder_tail", _lib.ptr(bufs["pooled"]), _lib.ptr(bufs["S"]), _lib.ptr(bufs["msum"]),
                   _lib.ptr(y), B, A * store.width, p.hidden, _lib.ptr(self.flat), self.offs_c, scale,
                   None, _lib.ptr(bufs["partial"]), rows, dev)
+        partial, prow = bufs["partial"], rows
+        if self.group is not None:
+            from .distributed import all_reduce_mean
+
+            _lib.call("wj_sum_partials", _lib.ptr(partial), rows, int(self.offs[-1]) + 1,
+                      _lib.ptr(self.grad_flat), dev)
+            all_reduce_mean(self.grad_flat, self.group)
+            partial, prow = self.grad_flat, 1
         _lib.call("wj_adam", _lib.ptr(self.flat), _lib.ptr(self.m_flat), _lib.ptr(self.v_flat),
-                  _lib.ptr(bufs["partial"]), rows, int(self.offs[-1]), st.lr, st.beta1, st.beta2,
+                  _lib.ptr(partial), prow, int(self.offs[-1]), st.lr, st.beta1, st.beta2,
                   st.eps, _lib.ptr(self.step_t), None, _lib.ptr(self.loss_buf), dev)
         return self.loss_buf[0]
 

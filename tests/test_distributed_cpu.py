@@ -36,7 +36,7 @@ def _worker(rank, world, port, q):
     try:
         from oracle import core
         from paper_2202_13538_b200.distributed import (all_gather_variable, all_reduce_grads,
-                                                       merge_distinct, shard_range)
+                                                       all_reduce_mean, merge_distinct, shard_range)
 
         # 1. variable-size all-gather
         t = torch.arange(3 + 4 * rank, dtype=torch.int64).reshape(-1, 1).repeat(1, 2) + 100 * rank
@@ -44,6 +44,13 @@ def _worker(rank, world, port, q):
         assert [p.shape[0] for p in parts] == [3 + 4 * r for r in range(world)]
         assert all(torch.equal(p, torch.arange(3 + 4 * r).reshape(-1, 1).repeat(1, 2) + 100 * r)
                    for r, p in enumerate(parts))
+
+        # int16 / uint16 store arrays travel as bytes (NCCL has no 16-bit integer type)
+        t16 = (torch.arange(2 + rank, dtype=torch.int16).reshape(-1, 1) * torch.tensor([1, -3], dtype=torch.int16))
+        parts16 = all_gather_variable(t16)
+        assert all(p.dtype == torch.int16 and torch.equal(p, torch.arange(2 + r, dtype=torch.int16).reshape(-1, 1)
+                                                          * torch.tensor([1, -3], dtype=torch.int16))
+                   for r, p in enumerate(parts16))
 
         # 2. sharded interning reproduces the reference table and ids
         g = load_golden("er1000_m50")
@@ -79,6 +86,10 @@ def _worker(rank, world, port, q):
         all_reduce_grads(grads, ["a", "b"])
         assert torch.allclose(grads["a"], torch.full((2, 3), 1.5))
         assert torch.allclose(grads["b"], torch.tensor([1.0]))
+        # 4. the fused step's flat [grads | loss] vector: mean over ranks in place
+        flat = torch.arange(5, dtype=torch.float32) * (rank + 1)
+        all_reduce_mean(flat)
+        assert torch.allclose(flat, torch.arange(5, dtype=torch.float32) * 1.5)
         q.put((rank, "ok"))
     except Exception as e:  # pragma: no cover - reported to the parent
         q.put((rank, repr(e)))
