@@ -54,6 +54,23 @@ __host__ __device__ __forceinline__ int bits_for(uint64_t v) {  // bits to hold 
     return b == 0 ? 1 : b;
 }
 
+// Ampere-style asynchronous global -> shared copies (LDGSTS): a thread issues
+// all of its staging copies back to back instead of serialising one L2
+// round trip per loop iteration.
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+                 "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+                 "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+                 "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 // per-thread error string for wj_last_error()
 void set_error(const char *fmt, ...);
 

@@ -120,6 +120,33 @@ __device__ __forceinline__ int lb_i32(const int32_t *a, int n, int32_t x) {
     return lo;
 }
 
+// Output word k of the staged row [x | 1 | 0...] (16 fp16 columns), where
+// column c < A*W is count f = c % W of anchor block j = c / W, taken from
+// the fp16 table row r[j] (W <= 8 halves in 4 words), column A*W is 1.0.
+// All selectors are compile-time constants after unrolling: one PRMT per word.
+template <int A, int W>
+__device__ __forceinline__ uint32_t half_src(const uint32_t (&r)[A][4], int c, int &sel_hi) {
+    constexpr int AW = A * W;
+    if (c < AW) {
+        const int j = c / W, f = c % W;
+        sel_hi = f & 1;
+        return r[j][f >> 1];
+    }
+    sel_hi = 0;
+    return c == AW ? 0x3C003C00u : 0u;
+}
+
+template <int A, int W>
+__device__ __forceinline__ void splice_row(const uint32_t (&r)[A][4], uint32_t (&out)[8]) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        int h0, h1;
+        const uint32_t x = half_src<A, W>(r, 2 * k, h0);
+        const uint32_t y = half_src<A, W>(r, 2 * k + 1, h1);
+        out[k] = __byte_perm(x, y, (h0 ? 0x32u : 0x10u) | ((h1 ? 0x76u : 0x54u) << 8));
+    }
+}
+
 template <int A, int AW>
 __global__ void __launch_bounds__(kMW * 32, 2) join_encode_mma_kernel(EncMmaArgs g) {
     static_assert(AW + 1 <= 16, "one k16 step: A*(L+1) + 1 <= 16");
@@ -139,8 +166,10 @@ __global__ void __launch_bounds__(kMW * 32, 2) join_encode_mma_kernel(EncMmaArgs
     int *un = reinterpret_cast<int *>(qa + 4);                       // U_a [4], prefix [4], heavy count, pad
     unsigned long long *wsum = reinterpret_cast<unsigned long long *>(un + 10);  // [warps + 2]
     float *wscale = reinterpret_cast<float *>(wsum + kMW + 2);       // [2]
-    uint64_t *tks = reinterpret_cast<uint64_t *>(wscale + 2);       // [tlen] (staged table)
-    int32_t *sx = reinterpret_cast<int32_t *>(tks + (g.stage_table ? g.tlen : 0));  // [A][mu]
+    uint64_t *tks = reinterpret_cast<uint64_t *>(wscale + 2);       // [tlen] (staged table keys)
+    uint4 *th = reinterpret_cast<uint4 *>(                          // [tlen] fp16 count rows
+        (reinterpret_cast<uintptr_t>(tks + ((g.stage_table & 1) ? g.tlen : 0)) + 15) & ~uintptr_t(15));
+    int32_t *sx = reinterpret_cast<int32_t *>(th + ((g.stage_table & 2) ? g.tlen : 0));  // [A][mu]
     int32_t *sid = sx + A * mu;                                      // [A][mu]
     int32_t *cross = sid + A * mu;                                   // [A][A-1][mu]
     uint32_t *vmap = reinterpret_cast<uint32_t *>(cross + A * (A - 1) * mu);  // [vcap]
@@ -178,11 +207,22 @@ __global__ void __launch_bounds__(kMW * 32, 2) join_encode_mma_kernel(EncMmaArgs
             wt[m * kXS + k] = hi;
             wt[H * kXS + m * kXS + k] = lo;
         }
-        if (g.stage_table)
-            for (int64_t i = threadIdx.x; i < g.tlen; i += NT) tks[i] = g.tkeys[i];
+        if (g.stage_table & 1) {
+            for (int64_t i = threadIdx.x; i < g.tlen; i += NT) cp_async8(tks + i, g.tkeys + i);
+            cp_async_wait_all();
+            __syncthreads();
+        }
+        if (g.stage_table & 2)  // each RPE vector as W fp16 counts (exact: counts <= 2048), zero padded
+            for (int64_t i = threadIdx.x; i < g.tlen; i += NT) {
+                const uint64_t key = tks[i];
+                float f[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) f[c] = c < W ? (float)(uint32_t)((key >> (g.cb * c)) & cmask) : 0.f;
+                th[i] = make_uint4(pack_h2(f[0], f[1]), pack_h2(f[2], f[3]), pack_h2(f[4], f[5]), pack_h2(f[6], f[7]));
+            }
         __syncthreads();
     }
-        const uint64_t *tkp = g.stage_table ? tks : g.tkeys;
+        const uint64_t *tkp = (g.stage_table & 1) ? tks : g.tkeys;
     __half *myx = xt + warp * 16 * kXS;
     float *myred = red + warp * H * kRedS;
 
@@ -207,10 +247,11 @@ __global__ void __launch_bounds__(kMW * 32, 2) join_encode_mma_kernel(EncMmaArgs
         for (int a = 0; a < A; ++a) {
             const int64_t lo = g.offsets[qa[a]];
             for (int i = threadIdx.x; i < un[a]; i += NT) {
-                sx[a * mu + i] = __ldg(g.ux + lo + i);
-                sid[a * mu + i] = __ldg(g.uid + lo + i);
+                cp_async4(sx + a * mu + i, g.ux + lo + i);
+                cp_async4(sid + a * mu + i, g.uid + lo + i);
             }
         }
+        cp_async_wait_all();
         __syncthreads();
         // RPE id of every landing of anchor a relative to every other anchor
 #pragma unroll
@@ -322,9 +363,7 @@ __global__ void __launch_bounds__(kMW * 32, 2) join_encode_mma_kernel(EncMmaArgs
             float my_t1 = 8388608.f, my_t2 = 8388608.f;
             if (lane < 16) {
                 const int v = v0 + lane;
-                float x[16];
-#pragma unroll
-                for (int c = 0; c < 16; ++c) x[c] = 0.f;
+                uint32_t wrow[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
                 if (v < V) {
                     const uint32_t e = vmap[v];
                     const int cnt = (int)(e & 3u);
@@ -335,32 +374,45 @@ __global__ void __launch_bounds__(kMW * 32, 2) join_encode_mma_kernel(EncMmaArgs
 #pragma unroll
                     for (int t = 1; t < A; ++t) a += lam >= un[4 + t];
                     const int l = lam - un[4 + a];
+                    int ids[A];
 #pragma unroll
                     for (int j = 0; j < A; ++j) {
-                        int id;
                         if (j == a) {
-                            id = sid[a * mu + l];
+                            ids[j] = sid[a * mu + l];
                         } else {
                             const int jj = j < a ? j : j - 1;
-                            id = cross[(a * (A - 1) + jj) * mu + l];
+                            ids[j] = cross[(a * (A - 1) + jj) * mu + l];
                         }
-                        const uint64_t key = tkp[id];
-#pragma unroll
-                        for (int c = 0; c < W; ++c) x[j * W + c] = (float)(uint32_t)((key >> (g.cb * c)) & cmask);
                     }
-                    x[AW] = 1.f;
+                    if (W <= 8 && (g.stage_table & 2)) {
+                        // fp16 rows from the staged table, spliced with byte permutes
+                        uint32_t r[A][4];
+#pragma unroll
+                        for (int j = 0; j < A; ++j) {
+                            const uint4 q4 = th[ids[j]];
+                            r[j][0] = q4.x;
+                            r[j][1] = q4.y;
+                            r[j][2] = q4.z;
+                            r[j][3] = q4.w;
+                        }
+                        splice_row<A, W>(r, wrow);
+                    } else {
+                        float x[16];
+#pragma unroll
+                        for (int c = 0; c < 16; ++c) x[c] = 0.f;
+#pragma unroll
+                        for (int j = 0; j < A; ++j) {
+                            const uint64_t key = tkp[ids[j]];
+#pragma unroll
+                            for (int c = 0; c < W; ++c) x[j * W + c] = (float)(uint32_t)((key >> (g.cb * c)) & cmask);
+                        }
+                        x[AW] = 1.f;
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) wrow[k] = pack_h2(x[2 * k], x[2 * k + 1]);
+                    }
                 }
-                uint4 lo4, hi4;
-                lo4.x = pack_h2(x[0], x[1]);
-                lo4.y = pack_h2(x[2], x[3]);
-                lo4.z = pack_h2(x[4], x[5]);
-                lo4.w = pack_h2(x[6], x[7]);
-                hi4.x = pack_h2(x[8], x[9]);
-                hi4.y = pack_h2(x[10], x[11]);
-                hi4.z = pack_h2(x[12], x[13]);
-                hi4.w = pack_h2(x[14], x[15]);
-                *reinterpret_cast<uint4 *>(myx + lane * kXS) = lo4;
-                *reinterpret_cast<uint4 *>(myx + lane * kXS + 8) = hi4;
+                *reinterpret_cast<uint4 *>(myx + lane * kXS) = make_uint4(wrow[0], wrow[1], wrow[2], wrow[3]);
+                *reinterpret_cast<uint4 *>(myx + lane * kXS + 8) = make_uint4(wrow[4], wrow[5], wrow[6], wrow[7]);
             }
             __syncwarp();
             // this thread's 4 landings: n = 8t + 2tq + s -> thresholds, hash bases
@@ -541,8 +593,12 @@ extern "C" int wj_join_encode(const int64_t *queries, int64_t n_batch, int32_t a
                   8 * (kMW + 2) + 8 + (size_t)arity * g.max_u * 8 + (size_t)arity * (arity - 1) * g.max_u * 4 +
                   (size_t)g.vcap * 4 + 16;
     const size_t limit = 200 * 1024;
-    g.stage_table = (base + (size_t)table_len * 8 <= 110 * 1024 && table_len <= 8192) ? 1 : 0;
-    const size_t smem = base + (g.stage_table ? (size_t)table_len * 8 : 0);
+    // stage the packed keys (bit 0) and, when they fit too, the fp16 count rows (bit 1)
+    const size_t budget = 110 * 1024;
+    g.stage_table = (base + (size_t)table_len * 8 <= budget && table_len <= 8192) ? 1 : 0;
+    if (g.stage_table && W <= 8 && base + (size_t)table_len * 24 + 16 <= budget) g.stage_table |= 2;
+    const size_t smem = base + ((g.stage_table & 1) ? (size_t)table_len * 8 : 0) +
+                        ((g.stage_table & 2) ? (size_t)table_len * 16 + 16 : 0);
     if (smem > limit) {
         set_error("join_encode needs %zu B of shared memory", smem);
         return WJ_ERR_UNSUPPORTED;

@@ -41,7 +41,13 @@ struct TailArgs {
     float scale;          // 1 / (keep * rows)
     float *logits;        // [B] nullable
     float *partial;       // [grid, total + 1] (last column: loss partial)
+    float *work;          // [B, kVecStride] per-query vectors (training)
+    int per_cta;          // queries per gradient CTA
 };
+
+// per-query vectors in the work buffer: pm, hq, dz2, dhq, g, a2*dl | dl, loss
+constexpr int kVecStride = 6 * kH + 8;
+enum { kPM = 0, kHQ = kH, kDZ2 = 2 * kH, kDHQ = 3 * kH, kG = 4 * kH, kA2DL = 5 * kH, kDL = 6 * kH, kLOSS };
 
 // out[c] = sum_k in[k] M[k][c] for the lane's columns c = lane, lane + 32
 // (in: the warp's 64-vector, lane holds k = lane, lane + 32).  Four
@@ -71,18 +77,18 @@ __device__ __forceinline__ void matvec_t(const float (&in)[2], const float *Ms, 
     for (int j = 0; j < 2; ++j) out[j] = (acc[j][0] + acc[j][1]) + (acc[j][2] + acc[j][3]);
 }
 
-template <int AW>
-__global__ void __launch_bounds__(kTailWarps * 32) encoder_tail_kernel(TailArgs g) {
+// Phase 1: one warp per query -- forward (logits) and, for training, the
+// per-query backward vectors into the work buffer.  No cross-query state.
+__global__ void __launch_bounds__(kTailWarps * 32) tail_vec_kernel(TailArgs g) {
     __shared__ float wts[2 * kH * kPitch];
     float *w2s = wts;
     float *u1s = wts + kH * kPitch;
-    __shared__ float vec[kTailWarps][4][kH];  // pm, hq, dz2, dhq of the group's queries
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const float *P = g.params;
     for (int i = threadIdx.x; i < kH * kH; i += blockDim.x) {
         const int r = i / kH, c = i % kH;
-        w2s[r * kPitch + c] = P[g.off.w2 + i];
-        u1s[r * kPitch + c] = P[g.off.u1 + i];
+        cp_async4(w2s + r * kPitch + c, P + g.off.w2 + i);
+        cp_async4(u1s + r * kPitch + c, P + g.off.u1 + i);
     }
     float b2v[2], c1v[2], u2v[2];
 #pragma unroll
@@ -92,167 +98,120 @@ __global__ void __launch_bounds__(kTailWarps * 32) encoder_tail_kernel(TailArgs 
         u2v[j] = P[g.off.u2 + lane + 32 * j];
     }
     const float c2 = P[g.off.c2];
-    const bool train = g.labels != nullptr;
-    // register accumulators
-    float dW1[AW][2], db1[2] = {0.f, 0.f}, du2[2] = {0.f, 0.f}, dc1[2] = {0.f, 0.f},
-                      db2[2] = {0.f, 0.f}, dc2 = 0.f, loss = 0.f;
-    float dU1[8][2], dW2[8][2];  // rows k = 8*warp + i, cols lane, lane+32
-#pragma unroll
-    for (int c = 0; c < AW; ++c) dW1[c][0] = dW1[c][1] = 0.f;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) dU1[i][0] = dU1[i][1] = dW2[i][0] = dW2[i][1] = 0.f;
+    cp_async_wait_all();
     __syncthreads();
     const float invB = 1.f / (float)g.B;
-    const int64_t groups = (g.B + kTailWarps - 1) / kTailWarps;
-    for (int64_t grp = blockIdx.x; grp < groups; grp += gridDim.x) {
-        const int64_t b = grp * kTailWarps + warp;
-        const bool active = b < g.B;
-        float pm[2] = {0.f, 0.f}, hq[2], dz2[2] = {0.f, 0.f}, dhq[2] = {0.f, 0.f};
-        if (active) {
+    for (int64_t b = (int64_t)blockIdx.x * kTailWarps + warp; b < g.B; b += (int64_t)gridDim.x * kTailWarps) {
+        float pm[2], hq[2], z2[2];
 #pragma unroll
-            for (int j = 0; j < 2; ++j) pm[j] = g.pooled[b * kH + lane + 32 * j] * g.scale;
-            matvec(pm, w2s, lane, hq);  // hq = pm W2 + b2
-            hq[0] += b2v[0];
-            hq[1] += b2v[1];
-            float z2[2];
-            matvec(hq, u1s, lane, z2);  // z2 = hq U1 + c1
-            z2[0] += c1v[0];
-            z2[1] += c1v[1];
-            const float a2[2] = {fmaxf(z2[0], 0.f), fmaxf(z2[1], 0.f)};
-            float part = a2[0] * u2v[0] + a2[1] * u2v[1];
+        for (int j = 0; j < 2; ++j) pm[j] = g.pooled[b * kH + lane + 32 * j] * g.scale;
+        matvec(pm, w2s, lane, hq);  // hq = pm W2 + b2
+        hq[0] += b2v[0];
+        hq[1] += b2v[1];
+        matvec(hq, u1s, lane, z2);  // z2 = hq U1 + c1
+        z2[0] += c1v[0];
+        z2[1] += c1v[1];
+        const float a2[2] = {fmaxf(z2[0], 0.f), fmaxf(z2[1], 0.f)};
+        float part = a2[0] * u2v[0] + a2[1] * u2v[1];
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
-            const float z = part + c2;
-            if (g.logits && lane == 0) g.logits[b] = z;
-            if (train) {
-                const float y = g.labels[b];
-                loss += fmaxf(z, 0.f) - z * y + log1pf(expf(-fabsf(z)));
-                const float sig = z >= 0.f ? 1.f / (1.f + expf(-z)) : expf(z) / (1.f + expf(z));
-                const float dl = (sig - y) * invB;
-                dc2 += dl;
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
+        const float z = part + c2;
+        if (g.logits && lane == 0) g.logits[b] = z;
+        if (!g.labels) continue;
+        const float y = g.labels[b];
+        const float loss = fmaxf(z, 0.f) - z * y + log1pf(expf(-fabsf(z)));
+        const float sig = z >= 0.f ? 1.f / (1.f + expf(-z)) : expf(z) / (1.f + expf(z));
+        const float dl = (sig - y) * invB;
+        float dz2[2], dhq[2], gk[2];
 #pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                    du2[j] = fmaf(a2[j], dl, du2[j]);
-                    dz2[j] = z2[j] > 0.f ? dl * u2v[j] : 0.f;
-                    dc1[j] += dz2[j];
-                }
-                // dhq[k] = sum_h dz2[h] U1[k][h], k = lane, lane + 32
-                matvec_t(dz2, u1s, lane, dhq);
-                db2[0] += dhq[0];
-                db2[1] += dhq[1];
-                // gk[k] = sum_h dhq[h] W2[k][h] * scale, k = lane, lane + 32
-                float gk[2];
-                matvec_t(dhq, w2s, lane, gk);
-                gk[0] *= g.scale;
-                gk[1] *= g.scale;
-#pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                    db1[j] = fmaf(g.msum[b * kH + lane + 32 * j], gk[j], db1[j]);
-#pragma unroll
-                    for (int c = 0; c < AW; ++c)
-                        dW1[c][j] = fmaf(g.s[(b * AW + c) * kH + lane + 32 * j], gk[j], dW1[c][j]);
-                }
-            }
-        }
-        if (!train) continue;
-        // rank-1 updates of dU1 = hq^T dz2 and dW2 = pm^T dhq, split by rows over warps
+        for (int j = 0; j < 2; ++j) dz2[j] = z2[j] > 0.f ? dl * u2v[j] : 0.f;
+        matvec_t(dz2, u1s, lane, dhq);  // dhq[k] = sum_h dz2[h] U1[k][h]
+        matvec_t(dhq, w2s, lane, gk);   // g[k] = sum_h dhq[h] W2[k][h] * scale
+        float *wk = g.work + b * kVecStride;
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-            vec[warp][0][lane + 32 * j] = pm[j];
-            vec[warp][1][lane + 32 * j] = active ? hq[j] : 0.f;
-            vec[warp][2][lane + 32 * j] = dz2[j];
-            vec[warp][3][lane + 32 * j] = dhq[j];
+            const int h = lane + 32 * j;
+            wk[kPM + h] = pm[j];
+            wk[kHQ + h] = hq[j];
+            wk[kDZ2 + h] = dz2[j];
+            wk[kDHQ + h] = dhq[j];
+            wk[kG + h] = gk[j] * g.scale;
+            wk[kA2DL + h] = a2[j] * dl;
         }
+        if (lane == 0) {
+            wk[kDL] = dl;
+            wk[kLOSS] = loss;
+        }
+    }
+}
+
+// Phase 2: CTA r reduces queries [r*per, (r+1)*per) in a fixed order into
+// partial row r.  Thread t owns column h = t % 64 of rows k = t/64 + 4i of
+// dW2 / dU1 / dW1 and one of the bias vectors; the chunk's vectors are staged
+// in shared memory, so the inner loop is pure FMA (no dependent chains).
+template <int AW>
+__global__ void __launch_bounds__(256) tail_grad_kernel(TailArgs g) {
+    constexpr int CH = 8;                   // queries per staged chunk
+    constexpr int NK = (AW + 3) / 4;        // dW1 rows per thread
+    __shared__ float wv[CH][kVecStride];
+    __shared__ float sv[CH][AW * kH + kH];  // S rows then msum
+    const int t = threadIdx.x, h = t & (kH - 1), kq = t >> 6;
+    float dW2[16], dU1[16], dW1[NK], vec = 0.f, dc2 = 0.f, loss = 0.f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) dW2[i] = dU1[i] = 0.f;
+#pragma unroll
+    for (int i = 0; i < NK; ++i) dW1[i] = 0.f;
+    const int64_t b0 = (int64_t)blockIdx.x * g.per_cta;
+    const int64_t b1 = min((int64_t)g.B, b0 + g.per_cta);
+    for (int64_t cb = b0; cb < b1; cb += CH) {
+        const int nq = (int)min((int64_t)CH, b1 - cb);
         __syncthreads();
-        for (int q = 0; q < kTailWarps; ++q) {
-            const float dzl[2] = {vec[q][2][lane], vec[q][2][lane + 32]};
-            const float dhl[2] = {vec[q][3][lane], vec[q][3][lane + 32]};
+        for (int i = t; i < nq * kVecStride; i += blockDim.x)
+            cp_async4(&wv[i / kVecStride][i % kVecStride], g.work + cb * kVecStride + i);
+        for (int i = t; i < nq * AW * kH; i += blockDim.x)
+            cp_async4(&sv[i / (AW * kH)][i % (AW * kH)], g.s + cb * AW * kH + i);
+        for (int i = t; i < nq * kH; i += blockDim.x) cp_async4(&sv[i / kH][AW * kH + i % kH], g.msum + cb * kH + i);
+        cp_async_wait_all();
+        __syncthreads();
+        for (int q = 0; q < nq; ++q) {
+            const float *w = wv[q];
+            const float dhq = w[kDHQ + h], dz2 = w[kDZ2 + h], gg = w[kG + h];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int k = warp * 8 + i;
-                const float hk = vec[q][1][k], pk = vec[q][0][k];
+            for (int i = 0; i < 16; ++i) {
+                dW2[i] = fmaf(w[kPM + kq + 4 * i], dhq, dW2[i]);
+                dU1[i] = fmaf(w[kHQ + kq + 4 * i], dz2, dU1[i]);
+            }
 #pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                    dU1[i][j] = fmaf(hk, dzl[j], dU1[i][j]);
-                    dW2[i][j] = fmaf(pk, dhl[j], dW2[i][j]);
-                }
+            for (int i = 0; i < NK; ++i)
+                if (kq + 4 * i < AW) dW1[i] = fmaf(sv[q][(kq + 4 * i) * kH + h], gg, dW1[i]);
+            if (kq == 0)
+                vec = fmaf(sv[q][AW * kH + h], gg, vec);  // db1
+            else if (kq == 1)
+                vec += dhq;                               // db2
+            else if (kq == 2)
+                vec += dz2;                               // dc1
+            else
+                vec += w[kA2DL + h];                      // du2
+            if (t == 0) {
+                dc2 += w[kDL];
+                loss += w[kLOSS];
             }
         }
-        __syncthreads();
     }
-    if (!train) return;
-    // this CTA's partial gradients -> its row of the partial buffer
     float *row = g.partial + (int64_t)blockIdx.x * (g.off.total + 1);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int k = warp * 8 + i;
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            row[g.off.u1 + k * kH + lane + 32 * j] = dU1[i][j];
-            row[g.off.w2 + k * kH + lane + 32 * j] = dW2[i][j];
-        }
-    }
-    // per-warp vectors: reduce over warps through shared memory (reusing the
-    // weight tiles, which are dead after the query loop), 8 vectors at a time
-    constexpr int NVEC = AW + 4;  // dW1 rows, db1, db2, dc1, du2
-    constexpr int CH = 8;
-    static_assert(kTailWarps * CH * kH <= 2 * kH * kPitch, "reduction tile too large");
-    float(*red)[CH][kH] = reinterpret_cast<float(*)[CH][kH]>(wts);
-    __shared__ float sred[kTailWarps][2];
-    float vals[NVEC][2];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-#pragma unroll
-        for (int c = 0; c < AW; ++c) vals[c][j] = dW1[c][j];
-        vals[AW + 0][j] = db1[j];
-        vals[AW + 1][j] = db2[j];
-        vals[AW + 2][j] = dc1[j];
-        vals[AW + 3][j] = du2[j];
-    }
-    if (lane == 0) {
-        sred[warp][0] = dc2;   // dc2 and the loss are warp-uniform: take lane 0
-        sred[warp][1] = loss;
+    for (int i = 0; i < 16; ++i) {
+        row[g.off.w2 + (kq + 4 * i) * kH + h] = dW2[i];
+        row[g.off.u1 + (kq + 4 * i) * kH + h] = dU1[i];
     }
 #pragma unroll
-    for (int v0 = 0; v0 < NVEC; v0 += CH) {
-        __syncthreads();
-#pragma unroll
-        for (int vv = 0; vv < CH; ++vv) {
-            if (v0 + vv < NVEC) {
-                red[warp][vv][lane] = vals[v0 + vv][0];
-                red[warp][vv][lane + 32] = vals[v0 + vv][1];
-            }
-        }
-        __syncthreads();
-        for (int i = threadIdx.x; i < CH * kH; i += blockDim.x) {
-            const int v = v0 + i / kH, h = i % kH;
-            if (v >= NVEC) continue;
-            float sum = 0.f;
-#pragma unroll
-            for (int w = 0; w < kTailWarps; ++w) sum += red[w][i / kH][h];
-            int dst;
-            if (v < AW)
-                dst = g.off.w1 + v * kH + h;
-            else if (v == AW)
-                dst = g.off.b1 + h;
-            else if (v == AW + 1)
-                dst = g.off.b2 + h;
-            else if (v == AW + 2)
-                dst = g.off.c1 + h;
-            else
-                dst = g.off.u2 + h;
-            row[dst] = sum;
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        float s = 0.f, l = 0.f;
-        for (int w = 0; w < kTailWarps; ++w) {
-            s += sred[w][0];
-            l += sred[w][1];
-        }
-        row[g.off.c2] = s;
-        row[g.off.total] = l * invB;
+    for (int i = 0; i < NK; ++i)
+        if (kq + 4 * i < AW) row[g.off.w1 + (kq + 4 * i) * kH + h] = dW1[i];
+    const int vo = kq == 0 ? g.off.b1 : (kq == 1 ? g.off.b2 : (kq == 2 ? g.off.c1 : g.off.u2));
+    row[vo + h] = vec;
+    if (t == 0) {
+        row[g.off.c2] = dc2;
+        row[g.off.total] = loss / (float)g.B;
     }
 }
 
@@ -317,7 +276,7 @@ using TailKernel = void (*)(TailArgs);
 static TailKernel pick_tail(int aw) {
     switch (aw) {
 #define WJ_T(x) \
-    case x: return encoder_tail_kernel<x>;
+    case x: return tail_grad_kernel<x>;
         WJ_T(2) WJ_T(3) WJ_T(4) WJ_T(5) WJ_T(6) WJ_T(8) WJ_T(9) WJ_T(10) WJ_T(12) WJ_T(14) WJ_T(15)
         WJ_T(16)
 #undef WJ_T
@@ -330,7 +289,7 @@ static TailKernel pick_tail(int aw) {
 extern "C" int wj_encoder_tail(const float *pooled, const float *s, const float *msum,
                                const float *labels, int64_t n_batch, int32_t aw, int32_t hidden,
                                const float *params, const int32_t *offsets9, float scale,
-                               float *logits_out, float *partial, int32_t partial_rows,
+                               float *logits_out, float *partial, int32_t partial_rows, float *work,
                                wj_stream_t stream) {
     using namespace wj;
     if (hidden != kH) {
@@ -342,8 +301,8 @@ extern "C" int wj_encoder_tail(const float *pooled, const float *s, const float 
         set_error("encoder tail not instantiated for A*(L+1)=%d", aw);
         return WJ_ERR_UNSUPPORTED;
     }
-    if (labels && (!s || !msum || !partial || partial_rows < 1)) {
-        set_error("training tail needs S, msum and a partial buffer");
+    if (labels && (!s || !msum || !partial || !work || partial_rows < 1)) {
+        set_error("training tail needs S, msum, a partial buffer and a work buffer");
         return WJ_ERR_ARG;
     }
     if (n_batch == 0) return WJ_OK;
@@ -359,10 +318,14 @@ extern "C" int wj_encoder_tail(const float *pooled, const float *s, const float 
     g.scale = scale;
     g.logits = logits_out;
     g.partial = partial;
+    g.work = work;
+    g.per_cta = (int)((n_batch + partial_rows - 1) / partial_rows);
     const int64_t groups = (n_batch + kTailWarps - 1) / kTailWarps;
-    int64_t grid = labels ? partial_rows : (groups < 1024 ? groups : 1024);
-    if (grid > groups && !labels) grid = groups;
-    k<<<(unsigned)grid, kTailWarps * 32, 0, (cudaStream_t)stream>>>(g);
+    const int64_t grid = groups < 4096 ? groups : 4096;
+    tail_vec_kernel<<<(unsigned)grid, kTailWarps * 32, 0, (cudaStream_t)stream>>>(g);
+    if (!labels) return check_launch("wj_encoder_tail");
+    // exactly partial_rows CTAs: rows past the last query write zeros
+    k<<<(unsigned)partial_rows, 256, 0, (cudaStream_t)stream>>>(g);
     return check_launch("wj_encoder_tail");
 }
 

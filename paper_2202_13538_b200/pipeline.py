@@ -250,12 +250,13 @@ class TrainStep:
     def _buffers(self, B, A):
         if self.mode == "fused":
             if self.fast_tail:
-                groups = (B + 7) // 8
-                rows = max(1, min(groups, self.tail_rows))
+                # gradient CTAs of 16 queries each (fixed-order partial rows)
+                rows = max(1, min((B + 15) // 16, self.tail_rows))
                 H, AW = self.params.hidden, A * self.store.width
                 return {"pooled": torch.empty((B, H), device=self.dev),
                         "S": torch.empty((B, AW, H), device=self.dev),
                         "msum": torch.empty((B, H), device=self.dev),
+                        "work": torch.empty((B, 6 * H + 8), device=self.dev),
                         "partial": torch.empty((rows, int(self.offs[-1]) + 1), device=self.dev)}
             H, AW = self.params.hidden, A * self.store.width
             return {"pooled": torch.empty((B, H), device=self.dev),
@@ -280,7 +281,7 @@ class TrainStep:
         rows = bufs["partial"].shape[0]
         _lib.call("wj_encoder_tail", _lib.ptr(bufs["pooled"]), _lib.ptr(bufs["S"]), _lib.ptr(bufs["msum"]),
                   _lib.ptr(y), B, A * store.width, p.hidden, _lib.ptr(self.flat), self.offs_c, scale,
-                  None, _lib.ptr(bufs["partial"]), rows, dev)
+                  None, _lib.ptr(bufs["partial"]), rows, _lib.ptr(bufs["work"]), dev)
         partial, prow = bufs["partial"], rows
         if self.group is not None:
             from .distributed import all_reduce_mean
