@@ -264,16 +264,11 @@ def run_ours(args, cfg):
                                   "msum": torch.empty((shp, 64), device=dev)})
     t_enc = None
     if A * (L + 1) <= 16:
-        from paper_2202_13538_b200 import _lib as L_
-
         def enc_launch(k):
             b = enc_bufs[qd[k].shape[0]]
             t = params.tensors
-            L_.call("wj_join_encode", L_.ptr(qd[k]), qd[k].shape[0], A, L_.ptr(store.offsets_d),
-                    L_.ptr(store.uniq_x_d), L_.ptr(store.uniq_id_d), M, L, store.max_unique,
-                    L_.ptr(store.table_keys_d), int(store.table_keys_d.numel()), L_.ptr(t["w1"]),
-                    L_.ptr(t["b1"]), 64, 0.9, 5, L_.ptr(step_t), L_.ptr(b["pooled"]), L_.ptr(b["S"]),
-                    L_.ptr(b["msum"]), L_.stream_handle(dev))
+            wj.encoder.join_encode(store, qd[k], t["w1"], t["b1"], 0.9, 5, step_t, b["pooled"], b["S"],
+                                   b["msum"])
 
         for k in range(W, W + K):
             enc_launch(k)

@@ -117,19 +117,45 @@ int wj_join(const int64_t *queries, int64_t n_batch, int32_t arity, const int32_
  *   msum_out[b, h]   = sum_r 1[z_r[h] > 0] * d_r[h]           (may be NULL)
  * with z_r = x_r W1 + b1 (w1 [A*(L+1), hidden] fp32, row-major), x_r the
  * joined RPE row of walk slot r and d_r a Bernoulli(keep_prob) dropout draw
- * from a counter-based stream keyed by (seed, *step, b, landing, unit)
- * (keep_prob = 1: no dropout).  *step is read on the device so a captured
- * CUDA graph advances it itself.  hidden = 64, A*(L+1) <= 15, M <= 2048 run
- * the tensor-core kernel (encode_mma.cu); other shapes the SIMT kernel
- * (wj_join_encode_simt).  Replaces _kernels.join_fill +
+ * from a counter-based stream keyed by (seed, *step, b, virtual landing,
+ * unit) (keep_prob = 1: no dropout).  *step is read on the device so a
+ * captured CUDA graph advances it itself.  voff / vcnt / vslots are the
+ * store's virtual-landing index (wj_vindex_count / wj_vindex_fill) and
+ * table_rows_f16 the fp16 table rows (wj_table_rows_f16); with them,
+ * hidden = 64, A*(L+1) <= 15, L+1 <= 8 and M <= 2048 run the tensor-core
+ * kernel (encode_mma.cu); otherwise (or if any of the four is NULL) the SIMT
+ * kernel (wj_join_encode_simt) runs.  Replaces _kernels.join_fill +
  * pipeline._dense_batch + the first layer of encoder.forward/backward
  * (_kernels.py:209-245, pipeline.py:169-182, encoder.py:150-161,224-232). */
 int wj_join_encode(const int64_t *queries, int64_t n_batch, int32_t arity, const int64_t *offsets,
-                   const int32_t *uniq_x, const int32_t *uniq_id, int32_t num_walks,
-                   int32_t num_steps, int32_t max_unique, const uint64_t *table_keys,
-                   int64_t table_len, const float *w1, const float *b1, int32_t hidden,
-                   float keep_prob, uint64_t seed, const int64_t *step, float *pooled_out,
-                   float *s_out, float *msum_out, wj_stream_t stream);
+                   const int32_t *uniq_x, const int32_t *uniq_id, const int64_t *voff,
+                   const int32_t *vcnt, const uint16_t *vslots, const uint16_t *table_rows_f16,
+                   int32_t num_walks, int32_t num_steps, int32_t max_unique,
+                   const uint64_t *table_keys, int64_t table_len, const float *w1, const float *b1,
+                   int32_t hidden, float keep_prob, uint64_t seed, const int64_t *step,
+                   float *pooled_out, float *s_out, float *msum_out, wj_stream_t stream);
+
+/* Virtual-landing index of a store (the encoder input layout; no reference
+ * counterpart -- it describes the rows pipeline._dense_batch builds,
+ * pipeline.py:169-182).  n_l = row sum of landing l's count vector = its
+ * number of rows in anchor u's block.  Count pass: vcnt_out[2u] =
+ * sum_l floor(n_l/2), vcnt_out[2u+1] = sum_l (n_l & 1).  Fill pass (voff =
+ * exclusive cumsum of vcnt[2u] + vcnt[2u+1], [n+1] int64): vslots_out
+ * [voff[u], voff[u] + vcnt[2u]) = l repeated floor(n_l/2) times, then every
+ * l with odd n_l once (uint16 landing indices into u's sorted list). */
+int wj_vindex_count(const int64_t *offsets, const int32_t *uniq_id, int64_t n_anchors,
+                    const uint64_t *table_keys, int32_t num_walks, int32_t num_steps,
+                    int32_t *vcnt_out, wj_stream_t stream);
+int wj_vindex_fill(const int64_t *offsets, const int32_t *uniq_id, int64_t n_anchors,
+                   const uint64_t *table_keys, int32_t num_walks, int32_t num_steps,
+                   const int64_t *voff, const int32_t *vcnt, uint16_t *vslots_out,
+                   wj_stream_t stream);
+
+/* fp16 rows of the RPE table: rows_out [table_len, 8] halves, counts of
+ * table row i in columns [0, L+1), zeros after (L+1 <= 8, M <= 2048: exact).
+ * The same vectors as store.table (store.py:33-46). */
+int wj_table_rows_f16(const uint64_t *table_keys, int64_t table_len, int32_t num_walks,
+                      int32_t num_steps, uint16_t *rows_out, wj_stream_t stream);
 
 /* Same contract on CUDA cores only (hidden in {32, 64, 128}, A*(L+1) <= 16);
  * its dropout stream differs from wj_join_encode's tensor-core kernel. */

@@ -13,7 +13,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "_walkjoin_b200.so")
-SOURCES = ["capi.cu", "sampler.cu", "rpe.cu", "intern.cu", "join.cu", "encode.cu", "encode_mma.cu", "tail.cu"]
+SOURCES = ["capi.cu", "sampler.cu", "rpe.cu", "intern.cu", "join.cu", "encode.cu", "encode_mma.cu", "tail.cu",
+           "vindex.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-O3", "-std=c++17", "-lineinfo", "--use_fast_math",
@@ -33,15 +34,32 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every source to an object in parallel, then link the shared
+    library (objects under build/, git-ignored)."""
     if not force and not _stale():
         return LIB
-    cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp",
-           *[os.path.join(CSRC, s) for s in SOURCES]]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd))
+    from concurrent.futures import ThreadPoolExecutor
+
+    objdir = os.path.join(ROOT, "build", "objs")
+    os.makedirs(objdir, exist_ok=True)
+    compile_flags = [f for f in FLAGS if f not in ("-shared", "-cudart", "static")]
     # nvcc picks the host compiler from PATH; keep it off a broken $CC
     env = dict(os.environ)
+
+    def compile_one(src):
+        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        cmd = [NVCC, *compile_flags, "-c", "-I", os.path.join(ROOT, "include"), "-o", obj,
+               os.path.join(CSRC, src)]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True, env=env)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
+           "-o", LIB + ".tmp", *objs]
     subprocess.run(cmd, check=True, env=env)
     os.replace(LIB + ".tmp", LIB)
     return LIB

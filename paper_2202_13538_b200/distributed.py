@@ -131,9 +131,12 @@ def preprocess_sharded(g, num_walks: int, num_steps: int, seed: int, threads: in
     ux = torch.cat(all_gather_variable(ux_l, group))
     uid = torch.cat(all_gather_variable(uid_l, group))
     uf = torch.cat(all_gather_variable(uf_l, group))
+    store = SubgraphStore(n, M, L, _u64(seed), walks, offsets, ux, uid, uf, slot, table_keys,
+                          int(counts.max().item()) if n else 0, id_map=getattr(g, "id_map", None))
+    ph.mark("vindex")
+    store.build_vindex()  # every rank holds the full store: no exchange needed
     ph.mark("end")
-    return SubgraphStore(n, M, L, _u64(seed), walks, offsets, ux, uid, uf, slot, table_keys,
-                         int(counts.max().item()) if n else 0, id_map=getattr(g, "id_map", None))
+    return store
 
 
 def all_reduce_mean(t: torch.Tensor, group=None) -> None:

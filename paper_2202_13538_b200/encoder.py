@@ -144,6 +144,25 @@ def forward(p: ModelParams, dense: torch.Tensor, training: bool = False,
     return logits, cache
 
 
+def join_encode(store, q: torch.Tensor, w1: torch.Tensor, b1: torch.Tensor, keep: float, seed: int,
+                step: Optional[torch.Tensor], pooled: torch.Tensor, S: Optional[torch.Tensor] = None,
+                msum: Optional[torch.Tensor] = None, simt: bool = False) -> None:
+    """One wj_join_encode launch (wj_join_encode_simt with ``simt``) on the
+    current stream; see include/walkjoin_b200.h for the outputs."""
+    from . import _lib
+
+    B, A = q.shape
+    args = (_lib.ptr(q), B, A, _lib.ptr(store.offsets_d), _lib.ptr(store.uniq_x_d), _lib.ptr(store.uniq_id_d))
+    tail = (store.num_walks, store.walk_steps, store.max_unique, _lib.ptr(store.table_keys_d),
+            int(store.table_keys_d.numel()), _lib.ptr(w1), _lib.ptr(b1), int(w1.shape[1]), float(keep),
+            int(seed) & ((1 << 64) - 1), _lib.ptr(step), _lib.ptr(pooled), _lib.ptr(S), _lib.ptr(msum),
+            _lib.stream_handle(store.device))
+    if simt:
+        _lib.call("wj_join_encode_simt", *args, *tail)
+    else:
+        _lib.call("wj_join_encode", *args, *store.vindex_ptrs(), *tail)
+
+
 def forward_fused(p: ModelParams, store, q: torch.Tensor, training: bool = False, seed: int = 0,
                   step: Optional[torch.Tensor] = None, need_grad: bool = True, out: dict = None,
                   tail: bool = True):
@@ -177,11 +196,7 @@ def forward_fused(p: ModelParams, store, q: torch.Tensor, training: bool = False
             S = torch.empty((B, AW, H), dtype=torch.float32, device=dev)
             msum = torch.empty((B, H), dtype=torch.float32, device=dev)
     t = p.tensors
-    _lib.call("wj_join_encode", _lib.ptr(q), B, A, _lib.ptr(store.offsets_d), _lib.ptr(store.uniq_x_d),
-              _lib.ptr(store.uniq_id_d), store.num_walks, store.walk_steps, store.max_unique,
-              _lib.ptr(store.table_keys_d), int(store.table_keys_d.numel()), _lib.ptr(t["w1"]),
-              _lib.ptr(t["b1"]), H, float(keep), int(seed) & ((1 << 64) - 1), _lib.ptr(step),
-              _lib.ptr(pooled), _lib.ptr(S), _lib.ptr(msum), _lib.stream_handle(dev))
+    join_encode(store, q, t["w1"], t["b1"], keep, seed, step, pooled, S, msum)
     if not tail:
         return None, None
     pooled_mean = pooled / (keep * rows)

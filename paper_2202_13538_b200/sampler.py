@@ -159,7 +159,7 @@ def preprocess(g, num_walks: int, num_steps: int, seed: int, threads: int = 1,
     """Build the device store (Alg. 1, reference sampler.py:94-151).
 
     ``phases`` (optional list) receives (name, start_event, end_event) per
-    phase: sample, rpe_count, rpe_fill, intern."""
+    phase: sample, rpe_count, rpe_fill, intern, vindex."""
     if num_walks < 1 or num_steps < 1:
         raise ValueError("num_walks and num_steps must be >= 1")
     if threads < 1:
@@ -195,9 +195,11 @@ def preprocess(g, num_walks: int, num_steps: int, seed: int, threads: int = 1,
               _lib.ptr(ukey), _lib.ptr(ufirst), _lib.ptr(slot), s)
     ph.mark("intern")
     uid, table_keys = intern_device(ukey, ufirst, offsets, n, 0, M, W)
-    ph.mark("end")
     store = SubgraphStore(n, M, L, seed64, walks, offsets, ux, uid, ufirst, slot, table_keys,
                           max_unique, id_map=getattr(g, "id_map", None))
+    ph.mark("vindex")
+    store.build_vindex()
+    ph.mark("end")
     if keep_keys:
         store.uniq_key_d = ukey
     return store

@@ -102,6 +102,39 @@ class SubgraphStore:
         self.device = walks_d.device
         self._anchor_counts = anchor_counts
         self._cache: dict = {}
+        self.voff_d = self.vcnt_d = self.vslots_d = self.trow_d = None
+
+    # ------------------------------------------- encoder input layout --
+    def build_vindex(self) -> None:
+        """Virtual-landing index (voff / vcnt / vslots) and fp16 table rows
+        that the tensor-core wj_join_encode reads (csrc/vindex.cu).  Built
+        once, right after interning; shapes outside that kernel's envelope
+        (L+1 > 8, M > 2048, M*(L+1) > 65535) get none and use the SIMT kernel."""
+        n, M, W = self.num_nodes, self.num_walks, self.width
+        if W > 8 or M > 2048 or M * W > 65535:
+            return
+        dev = self.device
+        s = _lib.stream_handle(dev)
+        vcnt = torch.empty((n, 2), dtype=torch.int32, device=dev)
+        _lib.call("wj_vindex_count", _lib.ptr(self.offsets_d), _lib.ptr(self.uniq_id_d), n,
+                  _lib.ptr(self.table_keys_d), M, self.walk_steps, _lib.ptr(vcnt), s)
+        voff = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+        if n:
+            torch.cumsum(vcnt.sum(1, dtype=torch.int64), 0, out=voff[1:])
+        total = int(voff[-1].item())
+        vslots = torch.empty(max(total, 1), dtype=torch.int16, device=dev)
+        _lib.call("wj_vindex_fill", _lib.ptr(self.offsets_d), _lib.ptr(self.uniq_id_d), n,
+                  _lib.ptr(self.table_keys_d), M, self.walk_steps, _lib.ptr(voff), _lib.ptr(vcnt),
+                  _lib.ptr(vslots), s)
+        T = int(self.table_keys_d.numel())
+        trow = torch.empty((max(T, 1), 8), dtype=torch.int16, device=dev)
+        _lib.call("wj_table_rows_f16", _lib.ptr(self.table_keys_d), T, M, self.walk_steps,
+                  _lib.ptr(trow), s)
+        self.voff_d, self.vcnt_d, self.vslots_d, self.trow_d = voff, vcnt, vslots, trow
+
+    def vindex_ptrs(self) -> tuple:
+        """(voff, vcnt, vslots, table_rows_f16) device pointers, or NULLs."""
+        return tuple(_lib.ptr(t) for t in (self.voff_d, self.vcnt_d, self.vslots_d, self.trow_d))
 
     # ---------------------------------------------------------- shapes --
     @property
@@ -222,7 +255,7 @@ class SubgraphStore:
         sizes["total"] = sum(sizes.values())
         sizes["device_index"] = sum(int(t.numel()) * t.element_size() for t in (
             self.offsets_d, self.uniq_x_d, self.uniq_id_d, self.uniq_first_d, self.slot_idx_d,
-            self.table_keys_d))
+            self.table_keys_d, self.voff_d, self.vcnt_d, self.vslots_d, self.trow_d) if t is not None)
         return sizes
 
     def _check_node(self, u: int):

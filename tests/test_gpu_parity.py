@@ -345,18 +345,22 @@ def _hash32(x):
     return x
 
 
-def _binomial_thresholds(keep):
+def _thresholds14(keep):
+    """14-bit inverse-CDF thresholds of the tensor-core kernel:
+    (1-row P(K>=1), 2-row P(K>=1), 2-row P(K>=2))."""
     k = float(np.float32(keep))
     if k >= 1.0:
-        return [(0, 0), (65536, 0), (65536, 65536)]
-    return [(0, 0), (int(k * 65536.0 + 0.5), 0),
-            (int((1.0 - (1.0 - k) * (1.0 - k)) * 65536.0 + 0.5), int(k * k * 65536.0 + 0.5))]
+        return 16384, 16384, 16384
+    t = lambda p: int(p * 16384.0 + 0.5)  # noqa: E731
+    return t(k), t(1.0 - (1.0 - k) * (1.0 - k)), t(k * k)
 
 
 def _fused_model_mma(store, q, w1, b1, keep, seed, step):
-    """Host model of the tensor-core wj_join_encode: virtual landings of <= 2
-    rows, Binomial(cnt, keep) kept rows by inverse CDF from the kernel's
-    hash32 stream; pooled / S / msum per query (float64)."""
+    """Host model of the tensor-core wj_join_encode: the query's virtual
+    landings in the store's vindex order (section 2: landing l repeated
+    floor(n_l/2) times per anchor, padded to 16; section 1: odd-n_l landings,
+    padded), Binomial(2, keep) / Bernoulli(keep) kept rows from the kernel's
+    14-bit hash stream; pooled / S / msum per query (float64)."""
     G = 0x9E3779B97F4A7C15
     off = store.offsets_d.cpu().numpy()
     ux = store.uniq_x_d.cpu().numpy()
@@ -365,17 +369,18 @@ def _fused_model_mma(store, q, w1, b1, keep, seed, step):
     B, A = q.shape
     W = store.width
     H = w1.shape[1]
-    thr = _binomial_thresholds(keep)
+    t11, t21, t22 = _thresholds14(keep)
     skey = _mix64((seed + G * (step + 1)) & _M64)
-    h = np.arange(H)
-    gq, mt, hb = h % 8, (h // 8) // 2, (h // 8) % 2
+    h = np.arange(H, dtype=np.uint64)
+    gq, hb, mt = h % 8, (h // 8) % 2, h // 16
     pooled = np.zeros((B, H))
     S = np.zeros((B, A * W, H))
     msum = np.zeros((B, H))
     for b in range(B):
-        qlo = _mix64(skey ^ _mix64(b)) & _M32
+        qq = _mix64(skey ^ _mix64(b)) & _M32
+        qq ^= qq >> 16
         lists = [(ux[off[q[b, j]]:off[q[b, j] + 1]], uid[off[q[b, j]]:off[q[b, j] + 1]]) for j in range(A)]
-        rows_x, cnts = [], []
+        sec2, sec1 = [], []
         for a in range(A):
             xa, ida = lists[a]
             ids = np.zeros((len(xa), A), np.int64)
@@ -390,26 +395,34 @@ def _fused_model_mma(store, q, w1, b1, keep, seed, step):
             X = T[ids].reshape(len(xa), A * W)
             n_l = T[ida].sum(1)
             for l in range(len(xa)):
-                r = int(n_l[l])
-                while r > 0:
-                    rows_x.append(X[l])
-                    cnts.append(min(r, 2))
-                    r -= 2
-        X = np.asarray(rows_x, np.float64)
-        cnt = np.asarray(cnts)
+                sec2 += [X[l]] * int(n_l[l] // 2)
+            for l in range(len(xa)):
+                if n_l[l] % 2:
+                    sec1.append(X[l])
+        zero = np.zeros(A * W, np.int64)
+        pad = lambda r: r + [zero] * ((-len(r)) % 16)  # noqa: E731
+        rows2, rows1 = pad(sec2), pad(sec1)
+        X = np.asarray(rows2 + rows1, np.float64).reshape(-1, A * W)
+        two = np.arange(X.shape[0]) < len(rows2)
         V = X.shape[0]
         z = (b1[None, :].astype(np.float64) + X @ w1.astype(np.float64)).astype(np.float32)
+        z[np.all(X == 0, axis=1)] = 0.0  # padding rows: contribute nothing
         v = np.arange(V, dtype=np.uint64)[:, None]
-        word = _hash32(np.uint64(qlo) ^ ((v << np.uint64(5)) | (gq[None, :].astype(np.uint64) << np.uint64(2))
-                                          | mt[None, :].astype(np.uint64)))
-        u = np.where(hb[None, :] == 1, word >> np.uint64(16), word & np.uint64(0xFFFF)).astype(np.int64)
-        t1 = np.array([thr[c][0] for c in cnt])[:, None]
-        t2 = np.array([thr[c][1] for c in cnt])[:, None]
-        kept = (u < t1).astype(np.float64) + (u < t2)
-        posm = z > 0
+        c = ((v >> np.uint64(1)) << np.uint64(6)) | (mt << np.uint64(4)) | (hb << np.uint64(3)) | gq
+        x = (np.uint64(qq) ^ c) & np.uint64(_M32)
+        x = (x * np.uint64(0x7FEB352D)) & np.uint64(_M32)
+        x ^= x >> np.uint64(15)
+        x = (x * np.uint64(0x846CA68B)) & np.uint64(_M32)
+        y = ~(x ^ (x >> np.uint64(16))) & np.uint64(0x3FFF3FFF)
+        lane = np.where((v & np.uint64(1)) == 1, y >> np.uint64(16), y & np.uint64(0xFFFF)).astype(np.int64)
+        u = 0x3FFF - lane
+        ta = np.where(two, t21, t11)[:, None]
+        tb = np.where(two, t22, 0)[:, None]
+        kept = (u < ta).astype(np.float64) + (u < tb)
+        posm = z >= 0
         pooled[b] = (np.where(posm, z, 0) * kept).sum(0)
         gk = posm * kept
-        msum[b] = gk.sum(0)
+        msum[b] = (gk * X.any(axis=1)[:, None]).sum(0)  # the bias column is 0 on padding rows
         S[b] = X.T @ gk
     return pooled, S, msum
 
@@ -429,11 +442,7 @@ def test_fused_join_encode_matches_host_model(wj, keep, kernel):
     S = torch.empty((12, 10, 64), device="cuda")
     msum = torch.empty((12, 64), device="cuda")
     qd = torch.from_numpy(q).cuda()
-    _lib.call("wj_join_encode" if kernel == "mma" else "wj_join_encode_simt", _lib.ptr(qd), 12, 2,
-              _lib.ptr(s.offsets_d), _lib.ptr(s.uniq_x_d), _lib.ptr(s.uniq_id_d), s.num_walks, s.walk_steps,
-              s.max_unique, _lib.ptr(s.table_keys_d), int(s.table_keys_d.numel()), _lib.ptr(p.w1),
-              _lib.ptr(p.b1), 64, float(keep), 99, _lib.ptr(step), _lib.ptr(pooled), _lib.ptr(S),
-              _lib.ptr(msum), _lib.stream_handle(torch.device("cuda", 0)))
+    wj.encoder.join_encode(s, qd, p.w1, p.b1, float(keep), 99, step, pooled, S, msum, simt=(kernel == "simt"))
     w1 = p.w1.cpu().numpy()
     b1 = p.b1.cpu().numpy()
     model = _fused_model_mma if kernel == "mma" else _fused_model
@@ -468,10 +477,7 @@ def test_dropout_stream_statistics(wj):
         ms = torch.empty((256, 64), device="cuda")
         pooled = torch.empty((256, 64), device="cuda")
         S = torch.empty((256, 10, 64), device="cuda")
-        _lib.call("wj_join_encode", _lib.ptr(q), 256, 2, _lib.ptr(s.offsets_d), _lib.ptr(s.uniq_x_d),
-                  _lib.ptr(s.uniq_id_d), s.num_walks, s.walk_steps, s.max_unique, _lib.ptr(s.table_keys_d),
-                  int(s.table_keys_d.numel()), _lib.ptr(p.w1), _lib.ptr(p.b1), 64, keep, 7, _lib.ptr(step),
-                  _lib.ptr(pooled), _lib.ptr(S), _lib.ptr(ms), _lib.stream_handle(torch.device("cuda", 0)))
+        wj.encoder.join_encode(s, q, p.w1, p.b1, keep, 7, step, pooled, S, ms)
         outs.append(ms.double().cpu().numpy())
     rows = 2 * s.landings
     k = np.stack(outs)  # [steps, B, 64] kept rows out of `rows`
