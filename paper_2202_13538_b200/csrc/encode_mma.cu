@@ -36,11 +36,12 @@
 // One CTA (8 warps) per query, persistent; each warp owns every 8th tile.
 #include <cuda_fp16.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace wj {
 
-constexpr int kMW = 8;        // warps per CTA
 constexpr int kWS = 24;       // halves per staged W^T row (48 B: conflict-free ldmatrix)
 constexpr int kRedS = 17;     // floats per unit in the reduction buffer (16 S^T cols + pad)
 constexpr int kRowB = 32;     // bytes per landing row [x | 1 | 0..] (16 halves)
@@ -198,8 +199,8 @@ __device__ __forceinline__ void tile(const uint16_t *lst, uint32_t xr_s, uint32_
     }
 }
 
-template <int A, int AW>
-__global__ void __launch_bounds__(kMW * 32, 2) join_encode_mma_kernel(EncMmaArgs g) {
+template <int A, int AW, int kMW, int MINB>
+__global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaArgs g) {
     static_assert(AW + 1 <= 16, "one k16 step: A*(L+1) + 1 <= 16");
     constexpr int W = AW / A;
     static_assert(W <= 8, "fp16 table rows hold 8 counts");
@@ -256,6 +257,7 @@ __global__ void __launch_bounds__(kMW * 32, 2) join_encode_mma_kernel(EncMmaArgs
         }
         __syncthreads();
     }
+
 
     for (int64_t b = blockIdx.x; b < g.n_batch; b += gridDim.x) {
         if (threadIdx.x < A) {
@@ -420,9 +422,10 @@ __global__ void __launch_bounds__(kMW * 32, 2) join_encode_mma_kernel(EncMmaArgs
 
 using EncMmaKernel = void (*)(EncMmaArgs);
 
+template <int NW, int MINB>
 static EncMmaKernel pick_mma(int A, int W) {
 #define WJ_CASE(a, w) \
-    if (A == a && W == w) return join_encode_mma_kernel<a, a * w>;
+    if (A == a && W == w) return join_encode_mma_kernel<a, a * w, NW, MINB>;
     WJ_CASE(1, 2) WJ_CASE(1, 3) WJ_CASE(1, 4) WJ_CASE(1, 5) WJ_CASE(1, 6) WJ_CASE(1, 7) WJ_CASE(1, 8)
     WJ_CASE(2, 2) WJ_CASE(2, 3) WJ_CASE(2, 4) WJ_CASE(2, 5) WJ_CASE(2, 6) WJ_CASE(2, 7)
     WJ_CASE(3, 2) WJ_CASE(3, 3) WJ_CASE(3, 4) WJ_CASE(3, 5)
@@ -456,6 +459,84 @@ extern "C" int wj_join_encode_simt(const int64_t *, int64_t, int32_t, const int6
                                    const float *, const float *, int32_t, float, uint64_t, const int64_t *,
                                    float *, float *, float *, wj_stream_t);
 
+namespace wj {
+
+// Kernel choice, shared-memory size and residency of the tensor-core kernel
+// for one shape; k == nullptr outside its envelope.
+struct MmaPlan {
+    EncMmaKernel k = nullptr;
+    int nw = 4;
+    size_t smem = 0;
+    int slots = 0;  // resident CTAs on the device (persistent grid)
+    int lcap = 0, xr_bytes = 0, mu = 1;
+};
+
+static int plan_mma(int arity, int num_walks, int num_steps, int max_unique, MmaPlan &pl) {
+    const int W = num_steps + 1;
+    // CTA shape: warps x min resident CTAs per SM (register budget); tuning
+    // override WJ_ENC_CFG in {"4x2", "4x3", "4x4", "8x2"}
+    static const char *env_cfg = getenv("WJ_ENC_CFG");
+    const int cfg = env_cfg ? (env_cfg[0] - '0') * 10 + (env_cfg[2] - '0') : 43;
+    if (num_walks > 2048) return WJ_ERR_UNSUPPORTED;
+    if (cfg == 42) pl.k = pick_mma<4, 2>(arity, W);
+    else if (cfg == 44) pl.k = pick_mma<4, 4>(arity, W);
+    else if (cfg == 82) { pl.k = pick_mma<8, 2>(arity, W); pl.nw = 8; }
+    else pl.k = pick_mma<4, 3>(arity, W);
+    if (!pl.k) return WJ_ERR_UNSUPPORTED;
+    const int64_t P = (int64_t)num_walks * W;
+    pl.mu = max_unique < 1 ? 1 : max_unique;
+    if (P > 65535 || (int64_t)arity * pl.mu + 1 > 65535) {
+        set_error("M*(L+1) or A*max_unique too large for uint16 row indices");
+        pl.k = nullptr;
+        return WJ_ERR_UNSUPPORTED;
+    }
+    // virtual landings per query: sum_a sum_l ceil(n_l / 2) <= A (P + U) / 2, + 2 x 15 padding
+    pl.lcap = (int)(((int64_t)arity * ((P + pl.mu) / 2 + 1) + 32 + 7) & ~7LL);
+    const int64_t rows_b = ((int64_t)arity * pl.mu + 1) * kRowB;
+    const int64_t red_b = (int64_t)pl.nw * 64 * kRedS * 4;
+    pl.xr_bytes = (int)(((rows_b > red_b ? rows_b : red_b) + 15) & ~15LL);
+    pl.smem = (size_t)kWtBytes + kHdrBytes + (size_t)pl.xr_bytes + (size_t)arity * pl.mu * 8 + (size_t)pl.lcap * 2;
+    if (pl.smem > 200 * 1024) {
+        set_error("join_encode needs %zu B of shared memory", pl.smem);
+        pl.k = nullptr;
+        return WJ_ERR_UNSUPPORTED;
+    }
+    cudaError_t e = cudaFuncSetAttribute(pl.k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+    if (e != cudaSuccess) {
+        set_error("join_encode smem attribute: %s", cudaGetErrorString(e));
+        pl.k = nullptr;
+        return WJ_ERR_CUDA;
+    }
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pl.k, pl.nw * 32, pl.smem);
+    pl.slots = sm_count() * (per_sm > 0 ? per_sm : 1);
+    return WJ_OK;
+}
+
+static void fill_args(EncMmaArgs &g, const MmaPlan &pl, const int64_t *queries, int64_t n_batch,
+                      const int64_t *offsets, const int32_t *uniq_x, const int32_t *uniq_id, const int64_t *voff,
+                      const int32_t *vcnt, const uint16_t *vslots, const uint16_t *table_rows_f16, float keep_prob,
+                      uint64_t seed, const int64_t *step) {
+    g = EncMmaArgs{};
+    g.queries = queries;
+    g.n_batch = n_batch;
+    g.offsets = offsets;
+    g.ux = uniq_x;
+    g.uid = uniq_id;
+    g.voff = voff;
+    g.vcnt = vcnt;
+    g.vslots = vslots;
+    g.trow = reinterpret_cast<const uint4 *>(table_rows_f16);
+    g.mu = pl.mu;
+    g.lcap = pl.lcap;
+    g.xr_bytes = pl.xr_bytes;
+    binomial_thresholds14(keep_prob, g.t11, g.t21, g.t22);
+    g.seed = seed;
+    g.step = step;
+}
+
+}  // namespace wj
+
 extern "C" int wj_join_encode(const int64_t *queries, int64_t n_batch, int32_t arity,
                               const int64_t *offsets, const int32_t *uniq_x,
                               const int32_t *uniq_id, const int64_t *voff, const int32_t *vcnt,
@@ -470,64 +551,31 @@ extern "C" int wj_join_encode(const int64_t *queries, int64_t n_batch, int32_t a
         set_error("bad arity / shape / keep_prob");
         return WJ_ERR_ARG;
     }
-    const int W = num_steps + 1;
-    EncMmaKernel k = (hidden == 64 && num_walks <= 2048 && voff && vcnt && vslots && table_rows_f16)
-                         ? pick_mma(arity, W)
-                         : nullptr;
-    if (!k)  // outside the tensor-core kernel's envelope (or no virtual-landing index)
+    MmaPlan pl;
+    const bool envelope = hidden == 64 && voff && vcnt && vslots && table_rows_f16;
+    int rc = envelope ? plan_mma(arity, num_walks, num_steps, max_unique, pl) : WJ_ERR_UNSUPPORTED;
+    if (rc == WJ_ERR_CUDA) return rc;
+    if (!pl.k)  // outside the tensor-core kernel's envelope (or no virtual-landing index)
         return wj_join_encode_simt(queries, n_batch, arity, offsets, uniq_x, uniq_id, num_walks, num_steps,
                                    max_unique, table_keys, table_len, w1, b1, hidden, keep_prob, seed, step,
                                    pooled_out, s_out, msum_out, stream);
-    const int64_t P = (int64_t)num_walks * W;
-    const int mu = max_unique < 1 ? 1 : max_unique;
-    if (P > 65535 || (int64_t)arity * mu + 1 > 65535) {
-        set_error("M*(L+1) or A*max_unique too large for uint16 row indices");
-        return WJ_ERR_UNSUPPORTED;
+    if (!pooled_out) {
+        set_error("pooled_out is required");
+        return WJ_ERR_ARG;
     }
     if (n_batch == 0) return WJ_OK;
     EncMmaArgs g;
-    g.queries = queries;
-    g.n_batch = n_batch;
-    g.offsets = offsets;
-    g.ux = uniq_x;
-    g.uid = uniq_id;
-    g.voff = voff;
-    g.vcnt = vcnt;
-    g.vslots = vslots;
-    g.trow = reinterpret_cast<const uint4 *>(table_rows_f16);
-    g.mu = mu;
-    // virtual landings per query: sum_a sum_l ceil(n_l / 2) <= A (P + U) / 2, + 2 x 15 padding
-    g.lcap = (int)(((int64_t)arity * ((P + mu) / 2 + 1) + 32 + 7) & ~7LL);
-    const int64_t rows_b = ((int64_t)arity * mu + 1) * kRowB;
-    const int64_t red_b = (int64_t)kMW * 64 * kRedS * 4;
-    g.xr_bytes = (int)(((rows_b > red_b ? rows_b : red_b) + 15) & ~15LL);
+    fill_args(g, pl, queries, n_batch, offsets, uniq_x, uniq_id, voff, vcnt, vslots, table_rows_f16, keep_prob,
+              seed, step);
     g.w1 = w1;
     g.b1 = b1;
-    binomial_thresholds14(keep_prob, g.t11, g.t21, g.t22);
-    g.seed = seed;
-    g.step = step;
     g.pooled = pooled_out;
     g.s_out = s_out;
     g.msum = msum_out;
-    const size_t smem = (size_t)kWtBytes + kHdrBytes + (size_t)g.xr_bytes + (size_t)arity * mu * 8 +
-                        (size_t)g.lcap * 2;
-    const size_t limit = 200 * 1024;
-    if (smem > limit) {
-        set_error("join_encode needs %zu B of shared memory", smem);
-        return WJ_ERR_UNSUPPORTED;
-    }
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) {
-        set_error("join_encode smem attribute: %s", cudaGetErrorString(e));
-        return WJ_ERR_CUDA;
-    }
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kMW * 32, smem);
     // persistent: one resident CTA slot per (SM, occupancy) -- W^T is split
     // once per CTA, not once per query
-    int64_t blocks = n_batch;
-    const int64_t cap = (int64_t)sm_count() * (per_sm > 0 ? per_sm : 1);
-    if (blocks > cap) blocks = cap;
-    k<<<(unsigned)blocks, kMW * 32, smem, (cudaStream_t)stream>>>(g);
+    const int64_t blocks = n_batch < pl.slots ? n_batch : pl.slots;
+    pl.k<<<(unsigned)blocks, pl.nw * 32, pl.smem, (cudaStream_t)stream>>>(g);
     return check_launch("wj_join_encode");
 }
+

@@ -222,6 +222,32 @@ __global__ void __launch_bounds__(256) tail_grad_kernel(TailArgs g) {
 // deterministic, and 8x the memory parallelism of one thread per column.
 constexpr int kAdamCols = 32, kAdamGroups = 8;
 
+// bias-corrected Adam on one parameter (encoder.py:236-249); explicit
+// roundings so every kernel that applies it produces the same bits
+__device__ __forceinline__ void adam_update(float *p, float *m, float *v, float g, float lr, float beta1,
+                                            float beta2, float eps, float bc1, float bc2) {
+    const float mi = __fadd_rn(__fmul_rn(beta1, *m), __fmul_rn(1.f - beta1, g));
+    const float vi = __fadd_rn(__fmul_rn(beta2, *v), __fmul_rn(__fmul_rn(1.f - beta2, g), g));
+    *m = mi;
+    *v = vi;
+    *p = __fsub_rn(*p, __fdiv_rn(__fmul_rn(lr, __fdiv_rn(mi, bc1)), __fadd_rn(__fsqrt_rn(__fdiv_rn(vi, bc2)), eps)));
+}
+
+// sum of p[r * ld] over rows r = grp, grp + 8, ... < rows: four independent
+// chains (four loads in flight), combined in a fixed order
+__device__ __forceinline__ float strided_sum(const float *p, int64_t ld, int grp, int rows) {
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    int r = grp;
+    for (; r + 3 * kAdamGroups < rows; r += 4 * kAdamGroups) {
+        s0 += p[(int64_t)r * ld];
+        s1 += p[(int64_t)(r + kAdamGroups) * ld];
+        s2 += p[(int64_t)(r + 2 * kAdamGroups) * ld];
+        s3 += p[(int64_t)(r + 3 * kAdamGroups) * ld];
+    }
+    for (; r < rows; r += kAdamGroups) s0 += p[(int64_t)r * ld];
+    return (s0 + s1) + (s2 + s3);
+}
+
 __global__ void __launch_bounds__(kAdamCols *kAdamGroups) adam_kernel(
     float *params, float *m, float *v, const float *partial, int rows, int n, float lr, float beta1,
     float beta2, float eps, const int64_t *step, float *grad_out, float *loss_out) {
@@ -229,8 +255,7 @@ __global__ void __launch_bounds__(kAdamCols *kAdamGroups) adam_kernel(
     const int c = threadIdx.x & (kAdamCols - 1), grp = threadIdx.x / kAdamCols;
     const int i = blockIdx.x * kAdamCols + c;
     float gsum = 0.f;
-    if (i <= n)
-        for (int r = grp; r < rows; r += kAdamGroups) gsum += partial[(int64_t)r * (n + 1) + i];
+    if (i <= n) gsum = strided_sum(partial + i, (int64_t)(n + 1), grp, rows);
     part[grp][c] = gsum;
     __syncthreads();
     if (grp != 0 || i > n) return;
@@ -245,11 +270,7 @@ __global__ void __launch_bounds__(kAdamCols *kAdamGroups) adam_kernel(
     const float bc1 = 1.f - powf(beta1, (float)t);
     const float bc2 = 1.f - powf(beta2, (float)t);
     if (grad_out) grad_out[i] = gsum;
-    const float mi = beta1 * m[i] + (1.f - beta1) * gsum;
-    const float vi = beta2 * v[i] + (1.f - beta2) * gsum * gsum;
-    m[i] = mi;
-    v[i] = vi;
-    params[i] -= lr * (mi / bc1) / (sqrtf(vi / bc2) + eps);
+    adam_update(params + i, m + i, v + i, gsum, lr, beta1, beta2, eps, bc1, bc2);
 }
 
 // Fixed-order column sums of the partial rows (the data-parallel path:
@@ -260,8 +281,7 @@ __global__ void __launch_bounds__(kAdamCols *kAdamGroups) sum_rows_kernel(const 
     const int c = threadIdx.x & (kAdamCols - 1), grp = threadIdx.x / kAdamCols;
     const int i = blockIdx.x * kAdamCols + c;
     float gsum = 0.f;
-    if (i < cols)
-        for (int r = grp; r < rows; r += kAdamGroups) gsum += partial[(int64_t)r * cols + i];
+    if (i < cols) gsum = strided_sum(partial + i, (int64_t)cols, grp, rows);
     part[grp][c] = gsum;
     __syncthreads();
     if (grp != 0 || i >= cols) return;

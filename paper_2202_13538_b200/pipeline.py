@@ -19,6 +19,7 @@ from typing import Optional, Sequence
 import numpy as np
 import torch
 
+from . import _lib
 from . import encoder as E
 from .joiner import dense_batch
 from .store import SubgraphStore
@@ -267,18 +268,17 @@ class TrainStep:
                                      dtype=self.dense_dtype, device=self.dev)}
 
     def _fast_body(self, q, y, bufs):
-        """fused kernel -> encoder tail kernel -> Adam kernel (3 launches)."""
+        """fused kernel -> encoder tail kernels -> Adam (4 launches)."""
         from . import _lib
 
         p, st, store = self.params, self.state, self.store
         B, A = q.shape
         self.step_t.add_(1)
-        E.forward_fused(p, store, q, training=True, seed=self.seed, step=self.step_t, out=bufs,
-                        tail=False)
         keep = (1.0 - p.dropout) if p.dropout > 0.0 else 1.0
         scale = 1.0 / (keep * A * store.landings)
         dev = _lib.stream_handle(self.dev)
         rows = bufs["partial"].shape[0]
+        E.forward_fused(p, store, q, training=True, seed=self.seed, step=self.step_t, out=bufs, tail=False)
         _lib.call("wj_encoder_tail", _lib.ptr(bufs["pooled"]), _lib.ptr(bufs["S"]), _lib.ptr(bufs["msum"]),
                   _lib.ptr(y), B, A * store.width, p.hidden, _lib.ptr(self.flat), self.offs_c, scale,
                   None, _lib.ptr(bufs["partial"]), rows, _lib.ptr(bufs["work"]), dev)
