@@ -171,16 +171,19 @@ int wj_join_encode_simt(const int64_t *queries, int64_t n_batch, int32_t arity,
  * pooled encodings (pm = pooled * scale), 2-layer classifier, BCE and the
  * full backward.  params is the flat fp32 parameter vector laid out by
  * offsets9 = {w1, b1, w2, b2, u1, c1, u2, c2, total}.  logits_out (may be
- * NULL) gets the [B] logits.  Training (labels != NULL) needs work
- * [n_batch, 392] floats (per-query backward vectors) and launches exactly
- * partial_rows gradient CTAs: CTA i reduces queries [i*q, (i+1)*q),
- * q = ceil(B / partial_rows), in a fixed order into partial[i, 0:total] and
- * its loss partial into partial[i, total].  Replaces encoder.forward /
- * bce_loss / backward after layer 1 (encoder.py:159-233). */
+ * NULL) gets the [B] logits.  Training (labels != NULL) launches exactly
+ * partial_rows CTAs: CTA i reduces queries [i*q, (i+1)*q), q = ceil(B /
+ * partial_rows) (best: partial_rows = ceil(B / 16)), in a fixed order into
+ * partial[i, 0:total] and its loss partial into partial[i, total].  work is
+ * unused (may be NULL).  step_inc (nullable) is incremented by one when the
+ * tail is done (the graph-resident step counter wj_join_encode and wj_adam
+ * read).  The [16 x 64] x [64 x 64] products run on the tensor cores in
+ * 3-pass TF32.  Replaces encoder.forward / bce_loss /
+ * backward after layer 1 (encoder.py:159-233). */
 int wj_encoder_tail(const float *pooled, const float *s, const float *msum, const float *labels,
                     int64_t n_batch, int32_t aw, int32_t hidden, const float *params,
                     const int32_t *offsets9, float scale, float *logits_out, float *partial,
-                    int32_t partial_rows, float *work, wj_stream_t stream);
+                    int32_t partial_rows, float *work, int64_t *step_inc, wj_stream_t stream);
 
 /* Deterministic reduction of the partial gradients + bias-corrected Adam
  * with t = *step (encoder.py:236-249).  grad_out / loss_out may be NULL. */

@@ -39,7 +39,7 @@ SIGNATURES = {
     "wj_table_rows_f16": [P, I64, I32, I32, P, P],
     "wj_join_encode_simt": [P, I64, I32, P, P, P, I32, I32, I32, P, I64, P, P, I32, ctypes.c_float, U64,
                             P, P, P, P, P],
-    "wj_encoder_tail": [P, P, P, P, I64, I32, I32, P, P, ctypes.c_float, P, P, I32, P, P],
+    "wj_encoder_tail": [P, P, P, P, I64, I32, I32, P, P, ctypes.c_float, P, P, I32, P, P, P],
     "wj_adam": [P, P, P, P, I32, I32, ctypes.c_float, ctypes.c_float, ctypes.c_float, ctypes.c_float,
                 P, P, P, P],
     "wj_sum_partials": [P, I32, I32, P, P],

@@ -46,7 +46,13 @@ constexpr int kWS = 24;       // halves per staged W^T row (48 B: conflict-free 
 constexpr int kRedS = 17;     // floats per unit in the reduction buffer (16 S^T cols + pad)
 constexpr int kRowB = 32;     // bytes per landing row [x | 1 | 0..] (16 halves)
 constexpr int kWtBytes = 2 * 64 * kWS * 2;
-constexpr int kHdrBytes = 256;
+constexpr int kRowU = 4;      // landings per thread per batch in the row build
+constexpr int kMetaQ = 16;    // queries whose metadata a CTA loads at once
+struct QMeta {
+    int64_t lo, vo;  // first entry of the anchor's sorted list / of its virtual landings
+    int u, v2, v1;   // list length, 2-row and 1-row virtual landings
+};
+constexpr int kHdrBytes = (kMetaQ * 3 * (int)sizeof(QMeta) + 16 + 15) & ~15;
 
 struct EncMmaArgs {
     const int64_t *queries;
@@ -59,6 +65,7 @@ struct EncMmaArgs {
     const uint16_t *vslots;
     const uint4 *trow;  // [tlen] fp16 count rows (8 halves)
     int mu, lcap, xr_bytes;
+    int lstep;  // largest power of two <= mu (binary-search stride)
     const float *w1;  // [AW, 64]
     const float *b1;  // [64]
     uint32_t t11, t21, t22;  // packed 14-bit thresholds (both lanes): 1-row; 2-row K>=1, K>=2
@@ -104,6 +111,16 @@ __device__ __forceinline__ uint32_t hadd2_u32(uint32_t a, uint32_t b) {
     uint32_t r;
     asm("add.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
     return r;
+}
+
+// a[i] for a runtime i < A without dynamic register indexing
+template <int A>
+__device__ __forceinline__ int pick(const int (&a)[A], int i) {
+    int v = a[0];
+#pragma unroll
+    for (int k = 1; k < A; ++k)
+        if (i == k) v = a[k];
+    return v;
 }
 
 __device__ __forceinline__ int lb_i32(const int32_t *a, int n, int32_t x) {
@@ -213,9 +230,8 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
 
     // ---- shared memory carve-up (16-B aligned blocks first)
     __half *wt = reinterpret_cast<__half *>(smem_raw);                 // [2][64][kWS] W^T hi / lo
-    int64_t *qlo = reinterpret_cast<int64_t *>(smem_raw + kWtBytes);    // [2A] list / vslot offsets
-    int *un = reinterpret_cast<int *>(qlo + 8);                         // [16] U_a, V2_a, V1_a
-    float *wscale = reinterpret_cast<float *>(un + 16);                 // [2]
+    QMeta *meta = reinterpret_cast<QMeta *>(smem_raw + kWtBytes);       // [kMetaQ][A] query metadata
+    float *wscale = reinterpret_cast<float *>(meta + kMetaQ * 3);       // [2]
     unsigned char *xr = smem_raw + kWtBytes + kHdrBytes;                // rows [A*mu + 1][32 B] | red
     float *red = reinterpret_cast<float *>(xr);                         // [warps][64][kRedS] (after tiles)
     int32_t *sx = reinterpret_cast<int32_t *>(xr + g.xr_bytes);         // [A][mu]
@@ -224,6 +240,7 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
     const uint32_t xr_s = smem_u32(xr), wt_s = smem_u32(wt);
     const uint32_t zrow = (uint32_t)(A * mu);  // all-zero row: padding (contributes nothing)
 
+    pdl_wait();  // params / step counter come from the previous kernel in the stream
     const uint64_t skey = mix64(g.seed + kGolden * ((uint64_t)(g.step ? *g.step : 0) + 1ULL));
 
     // ---- W^T = [W1; b1; 0]^T as a power-of-two-scaled fp16 hi + lo pair
@@ -259,25 +276,37 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
     }
 
 
-    for (int64_t b = blockIdx.x; b < g.n_batch; b += gridDim.x) {
-        if (threadIdx.x < A) {
-            const int a = threadIdx.x;
-            const int64_t q = g.queries[b * A + a];
-            const int64_t lo = g.offsets[q];
-            qlo[a] = lo;
-            qlo[A + a] = g.voff[q];
-            un[a] = (int)(g.offsets[q + 1] - lo);
-            un[4 + a] = g.vcnt[2 * q];
-            un[8 + a] = g.vcnt[2 * q + 1];
+    int jq = 0;  // local query index
+    for (int64_t b = blockIdx.x; b < g.n_batch; b += gridDim.x, ++jq) {
+        if (b + gridDim.x >= g.n_batch) pdl_trigger();  // last query of this CTA: dependents may launch
+        if (jq % kMetaQ == 0) {
+            // metadata of this CTA's next kMetaQ queries, loaded in one go
+            // (q -> offsets / vindex is a dependent pair of global reads)
+            __syncthreads();
+            for (int t = threadIdx.x; t < kMetaQ * A; t += NT) {
+                const int i = t / A, a = t - i * A;
+                const int64_t bb = b + (int64_t)i * gridDim.x;
+                QMeta m = {0, 0, 0, 0, 0};
+                if (bb < g.n_batch) {
+                    const int64_t q = g.queries[bb * A + a];
+                    m.lo = g.offsets[q];
+                    m.u = (int)(g.offsets[q + 1] - m.lo);
+                    m.vo = g.voff[q];
+                    m.v2 = g.vcnt[2 * q];
+                    m.v1 = g.vcnt[2 * q + 1];
+                }
+                meta[t] = m;
+            }
+            __syncthreads();
         }
-        __syncthreads();
+        const QMeta *qm = meta + (jq % kMetaQ) * A;
         int U[A], V2[A], V1[A], pu[A + 1], p2[A + 1], p1[A + 1];
         pu[0] = p2[0] = p1[0] = 0;
 #pragma unroll
         for (int a = 0; a < A; ++a) {
-            U[a] = un[a];
-            V2[a] = un[4 + a];
-            V1[a] = un[8 + a];
+            U[a] = qm[a].u;
+            V2[a] = qm[a].v2;
+            V1[a] = qm[a].v1;
             pu[a + 1] = pu[a] + U[a];
             p2[a + 1] = p2[a] + V2[a];
             p1[a + 1] = p1[a] + V1[a];
@@ -286,8 +315,8 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
         // ---- stage the anchors' sorted lists (async) and the virtual-landing rows
 #pragma unroll
         for (int a = 0; a < A; ++a) {
-            const int32_t *gx = g.ux + qlo[a];
-            const int32_t *gi = g.uid + qlo[a];
+            const int32_t *gx = g.ux + qm[a].lo;
+            const int32_t *gi = g.uid + qm[a].lo;
             for (int i = threadIdx.x; i < U[a]; i += NT) {
                 cp_async4(sx + a * mu + i, gx + i);
                 cp_async4(sid + a * mu + i, gi + i);
@@ -295,7 +324,7 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
         }
 #pragma unroll
         for (int a = 0; a < A; ++a) {
-            const uint16_t *vs = g.vslots + qlo[A + a];
+            const uint16_t *vs = g.vslots + qm[a].vo;
             const uint16_t add = (uint16_t)(a * mu);
             for (int i = threadIdx.x; i < V2[a]; i += NT) vl[p2[a] + i] = (uint16_t)(__ldg(vs + i) + add);
             for (int i = threadIdx.x; i < V1[a]; i += NT) vl[P2 + p1[a] + i] = (uint16_t)(__ldg(vs + V2[a] + i) + add);
@@ -306,55 +335,84 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
         cp_async_wait_all();
         __syncthreads();
 
-        // ---- one fp16 row per distinct landing: thread t owns a contiguous
-        // chunk of the concatenated lists; the RPE id of landing x relative
-        // to anchor j != a comes from a binary search for the chunk's first
-        // landing, then a forward merge (both lists are sorted)
+        // ---- one fp16 row per distinct landing.  Thread t owns landings
+        // e = t, t + NT, ... of the concatenated lists; the RPE id of landing
+        // x relative to anchor j != a is a fixed-step (branch-free) binary
+        // search of x in j's sorted list, kRowU landings at a time so the
+        // searches and the fp16 table-row loads overlap
         {
             const int LT = pu[A];
-            const int per = (LT + NT - 1) / NT;
-            const int e0 = min((int)threadIdx.x * per, LT), e1 = min(e0 + per, LT);
-            int pos[A];
-            int cur = -1;
-            for (int e = e0; e < e1; ++e) {
-                int a = 0;
+            for (int e0 = threadIdx.x; e0 < LT; e0 += kRowU * NT) {
+                int ids[kRowU][A], rowi[kRowU], la[kRowU], xs[kRowU], own[kRowU], pos[kRowU][A];
 #pragma unroll
-                for (int t = 1; t < A; ++t) a += e >= pu[t];
-                int base_a = 0;
+                for (int u = 0; u < kRowU; ++u) {
+                    const int e = e0 + u * NT;
+                    const bool ok = e < LT;
+                    int a = 0;
 #pragma unroll
-                for (int t = 1; t < A; ++t)
-                    if (a == t) base_a = pu[t];
-                const int l = e - base_a;
-                const int32_t x = sx[a * mu + l];
-                uint32_t r[A][4];
+                    for (int t = 1; t < A; ++t) a += e >= pu[t];
+                    int base_a = 0;
 #pragma unroll
-                for (int j = 0; j < A; ++j) {
-                    int id;
-                    if (j == a) {
-                        id = sid[a * mu + l];
-                    } else {
-                        const int32_t *xj = sx + j * mu;
-                        const int nj = U[j];
-                        if (a != cur) {
-                            pos[j] = lb_i32(xj, nj, x);
-                        } else {
-                            while (pos[j] < nj && xj[pos[j]] < x) ++pos[j];
-                        }
-                        id = (pos[j] < nj && xj[pos[j]] == x) ? sid[j * mu + pos[j]] : 0;
-                    }
-                    const uint4 q4 = __ldg(g.trow + id);
-                    r[j][0] = q4.x;
-                    r[j][1] = q4.y;
-                    r[j][2] = q4.z;
-                    r[j][3] = q4.w;
+                    for (int t = 1; t < A; ++t)
+                        if (a == t) base_a = pu[t];
+                    const int l = ok ? e - base_a : 0;
+                    la[u] = a;
+                    rowi[u] = ok ? a * mu + l : -1;
+                    xs[u] = sx[a * mu + l];
+                    own[u] = sid[a * mu + l];
+#pragma unroll
+                    for (int jj = 0; jj < A; ++jj) pos[u][jj] = 0;
                 }
-                cur = a;
-                uint32_t w[8];
-                splice_row<A, W>(r, w);
-                const uint32_t row = (uint32_t)(a * mu + l);
-                const uint32_t sw = (row >> 2) & 1u;
-                *reinterpret_cast<uint4 *>(xr + row * kRowB + (sw << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
-                *reinterpret_cast<uint4 *>(xr + row * kRowB + ((sw ^ 1u) << 4)) = make_uint4(w[4], w[5], w[6], w[7]);
+                // searches of x in the other anchors' lists, all (u, j) in lock step
+#pragma unroll
+                for (int sh = 15; sh >= 0; --sh) {
+                    const int step = 1 << sh;
+                    if (step > g.lstep) continue;
+#pragma unroll
+                    for (int u = 0; u < kRowU; ++u)
+#pragma unroll
+                        for (int jj = 0; jj < A - 1; ++jj) {
+                            const int j = jj < la[u] ? jj : jj + 1;
+                            const int p = pos[u][jj] + step;
+                            if (p <= pick<A>(U, j) && sx[j * mu + p - 1] < xs[u]) pos[u][jj] = p;
+                        }
+                }
+#pragma unroll
+                for (int u = 0; u < kRowU; ++u)
+#pragma unroll
+                    for (int j = 0; j < A; ++j) {
+                        const int jj = j < la[u] ? j : j - 1;
+                        int pp = 0;
+#pragma unroll
+                        for (int k = 0; k < A - 1; ++k)
+                            if (k == jj) pp = pos[u][k];
+                        const int pc = min(pp, mu - 1);
+                        const int cross = (pp < U[j] && sx[j * mu + pc] == xs[u]) ? sid[j * mu + pc] : 0;
+                        ids[u][j] = j == la[u] ? own[u] : cross;
+                    }
+                uint4 t4[kRowU][A];
+#pragma unroll
+                for (int u = 0; u < kRowU; ++u)
+#pragma unroll
+                    for (int j = 0; j < A; ++j) t4[u][j] = __ldg(g.trow + (rowi[u] >= 0 ? ids[u][j] : 0));
+#pragma unroll
+                for (int u = 0; u < kRowU; ++u) {
+                    if (rowi[u] < 0) continue;
+                    uint32_t r[A][4];
+#pragma unroll
+                    for (int j = 0; j < A; ++j) {
+                        r[j][0] = t4[u][j].x;
+                        r[j][1] = t4[u][j].y;
+                        r[j][2] = t4[u][j].z;
+                        r[j][3] = t4[u][j].w;
+                    }
+                    uint32_t w[8];
+                    splice_row<A, W>(r, w);
+                    const uint32_t row = (uint32_t)rowi[u];
+                    const uint32_t sw = (row >> 2) & 1u;
+                    *reinterpret_cast<uint4 *>(xr + row * kRowB + (sw << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+                    *reinterpret_cast<uint4 *>(xr + row * kRowB + ((sw ^ 1u) << 4)) = make_uint4(w[4], w[5], w[6], w[7]);
+                }
             }
         }
         __syncthreads();
@@ -528,6 +586,8 @@ static void fill_args(EncMmaArgs &g, const MmaPlan &pl, const int64_t *queries, 
     g.vslots = vslots;
     g.trow = reinterpret_cast<const uint4 *>(table_rows_f16);
     g.mu = pl.mu;
+    g.lstep = 1;
+    while (g.lstep * 2 <= pl.mu) g.lstep *= 2;
     g.lcap = pl.lcap;
     g.xr_bytes = pl.xr_bytes;
     binomial_thresholds14(keep_prob, g.t11, g.t21, g.t22);
@@ -575,7 +635,11 @@ extern "C" int wj_join_encode(const int64_t *queries, int64_t n_batch, int32_t a
     // persistent: one resident CTA slot per (SM, occupancy) -- W^T is split
     // once per CTA, not once per query
     const int64_t blocks = n_batch < pl.slots ? n_batch : pl.slots;
-    pl.k<<<(unsigned)blocks, pl.nw * 32, pl.smem, (cudaStream_t)stream>>>(g);
+    const cudaError_t e = launch_pdl(pl.k, dim3((unsigned)blocks), dim3(pl.nw * 32), pl.smem, (cudaStream_t)stream, g);
+    if (e != cudaSuccess) {
+        set_error("wj_join_encode launch: %s", cudaGetErrorString(e));
+        return WJ_ERR_CUDA;
+    }
     return check_launch("wj_join_encode");
 }
 

@@ -11,13 +11,12 @@
 //   dlogit = (sigmoid(z) - y) / B,  dz2 = dlogit u2 * 1[z2 > 0]
 //   dhq = dz2 U1^T,  g = (dhq W2^T) * scale
 //   dW2 += pm^T dhq, dU1 += hq^T dz2, dW1 += S_b * g, db1 += msum_b * g
-// One warp per query (lane owns hidden units lane and lane+32: conflict-free
-// shared-memory access to both W and W^T with a 65-float row pitch); the
-// rank-1 updates of the 64x64 gradients are split by rows across the CTA's 8
-// warps.  Each CTA writes its partial gradients to its own row of a
-// [grid, n_params] buffer; the Adam kernel reduces those rows in a fixed
-// order (deterministic) and applies the bias-corrected update
-// (encoder.py:236-249).
+// tail_tc_kernel: one CTA per chunk of 16 queries runs every [16 x 64] x
+// [64 x 64] product above (and the rank-16 gradient updates) on the tensor
+// cores in 3-pass TF32 (fp32-level accuracy) and writes its partial
+// gradients to its own row of a [grid, n_params + 1] buffer; the Adam kernel
+// reduces those rows in a fixed order (deterministic) and applies the
+// bias-corrected update (encoder.py:236-249).
 #include "common.cuh"
 
 namespace wj {
@@ -39,181 +38,13 @@ struct TailArgs {
     const float *params;
     ParamOffsets off;
     float scale;          // 1 / (keep * rows)
+    float inv_b;          // 1 / B (mean BCE)
+    int64_t *step_inc;    // incremented once the tail is done (nullable)
     float *logits;        // [B] nullable
     float *partial;       // [grid, total + 1] (last column: loss partial)
     float *work;          // [B, kVecStride] per-query vectors (training)
     int per_cta;          // queries per gradient CTA
 };
-
-// per-query vectors in the work buffer: pm, hq, dz2, dhq, g, a2*dl | dl, loss
-constexpr int kVecStride = 6 * kH + 8;
-enum { kPM = 0, kHQ = kH, kDZ2 = 2 * kH, kDHQ = 3 * kH, kG = 4 * kH, kA2DL = 5 * kH, kDL = 6 * kH, kLOSS };
-
-// out[c] = sum_k in[k] M[k][c] for the lane's columns c = lane, lane + 32
-// (in: the warp's 64-vector, lane holds k = lane, lane + 32).  Four
-// independent accumulator chains per output instead of one 64-long chain.
-__device__ __forceinline__ void matvec(const float (&in)[2], const float *Ms, int lane, float (&out)[2]) {
-    float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-#pragma unroll
-    for (int k = 0; k < kH; ++k) {
-        const float x = __shfl_sync(kFull, in[k >> 5], k & 31);
-        acc[0][k & 3] = fmaf(x, Ms[k * kPitch + lane], acc[0][k & 3]);
-        acc[1][k & 3] = fmaf(x, Ms[k * kPitch + lane + 32], acc[1][k & 3]);
-    }
-#pragma unroll
-    for (int j = 0; j < 2; ++j) out[j] = (acc[j][0] + acc[j][1]) + (acc[j][2] + acc[j][3]);
-}
-
-// out[r] = sum_h in[h] M[r][h] for the lane's rows r = lane, lane + 32
-__device__ __forceinline__ void matvec_t(const float (&in)[2], const float *Ms, int lane, float (&out)[2]) {
-    float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-#pragma unroll
-    for (int h = 0; h < kH; ++h) {
-        const float x = __shfl_sync(kFull, in[h >> 5], h & 31);
-        acc[0][h & 3] = fmaf(x, Ms[lane * kPitch + h], acc[0][h & 3]);
-        acc[1][h & 3] = fmaf(x, Ms[(lane + 32) * kPitch + h], acc[1][h & 3]);
-    }
-#pragma unroll
-    for (int j = 0; j < 2; ++j) out[j] = (acc[j][0] + acc[j][1]) + (acc[j][2] + acc[j][3]);
-}
-
-// Phase 1: one warp per query -- forward (logits) and, for training, the
-// per-query backward vectors into the work buffer.  No cross-query state.
-__global__ void __launch_bounds__(kTailWarps * 32) tail_vec_kernel(TailArgs g) {
-    __shared__ float wts[2 * kH * kPitch];
-    float *w2s = wts;
-    float *u1s = wts + kH * kPitch;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const float *P = g.params;
-    for (int i = threadIdx.x; i < kH * kH; i += blockDim.x) {
-        const int r = i / kH, c = i % kH;
-        cp_async4(w2s + r * kPitch + c, P + g.off.w2 + i);
-        cp_async4(u1s + r * kPitch + c, P + g.off.u1 + i);
-    }
-    float b2v[2], c1v[2], u2v[2];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        b2v[j] = P[g.off.b2 + lane + 32 * j];
-        c1v[j] = P[g.off.c1 + lane + 32 * j];
-        u2v[j] = P[g.off.u2 + lane + 32 * j];
-    }
-    const float c2 = P[g.off.c2];
-    cp_async_wait_all();
-    __syncthreads();
-    const float invB = 1.f / (float)g.B;
-    for (int64_t b = (int64_t)blockIdx.x * kTailWarps + warp; b < g.B; b += (int64_t)gridDim.x * kTailWarps) {
-        float pm[2], hq[2], z2[2];
-#pragma unroll
-        for (int j = 0; j < 2; ++j) pm[j] = g.pooled[b * kH + lane + 32 * j] * g.scale;
-        matvec(pm, w2s, lane, hq);  // hq = pm W2 + b2
-        hq[0] += b2v[0];
-        hq[1] += b2v[1];
-        matvec(hq, u1s, lane, z2);  // z2 = hq U1 + c1
-        z2[0] += c1v[0];
-        z2[1] += c1v[1];
-        const float a2[2] = {fmaxf(z2[0], 0.f), fmaxf(z2[1], 0.f)};
-        float part = a2[0] * u2v[0] + a2[1] * u2v[1];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
-        const float z = part + c2;
-        if (g.logits && lane == 0) g.logits[b] = z;
-        if (!g.labels) continue;
-        const float y = g.labels[b];
-        const float loss = fmaxf(z, 0.f) - z * y + log1pf(expf(-fabsf(z)));
-        const float sig = z >= 0.f ? 1.f / (1.f + expf(-z)) : expf(z) / (1.f + expf(z));
-        const float dl = (sig - y) * invB;
-        float dz2[2], dhq[2], gk[2];
-#pragma unroll
-        for (int j = 0; j < 2; ++j) dz2[j] = z2[j] > 0.f ? dl * u2v[j] : 0.f;
-        matvec_t(dz2, u1s, lane, dhq);  // dhq[k] = sum_h dz2[h] U1[k][h]
-        matvec_t(dhq, w2s, lane, gk);   // g[k] = sum_h dhq[h] W2[k][h] * scale
-        float *wk = g.work + b * kVecStride;
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            const int h = lane + 32 * j;
-            wk[kPM + h] = pm[j];
-            wk[kHQ + h] = hq[j];
-            wk[kDZ2 + h] = dz2[j];
-            wk[kDHQ + h] = dhq[j];
-            wk[kG + h] = gk[j] * g.scale;
-            wk[kA2DL + h] = a2[j] * dl;
-        }
-        if (lane == 0) {
-            wk[kDL] = dl;
-            wk[kLOSS] = loss;
-        }
-    }
-}
-
-// Phase 2: CTA r reduces queries [r*per, (r+1)*per) in a fixed order into
-// partial row r.  Thread t owns column h = t % 64 of rows k = t/64 + 4i of
-// dW2 / dU1 / dW1 and one of the bias vectors; the chunk's vectors are staged
-// in shared memory, so the inner loop is pure FMA (no dependent chains).
-template <int AW>
-__global__ void __launch_bounds__(256) tail_grad_kernel(TailArgs g) {
-    constexpr int CH = 8;                   // queries per staged chunk
-    constexpr int NK = (AW + 3) / 4;        // dW1 rows per thread
-    __shared__ float wv[CH][kVecStride];
-    __shared__ float sv[CH][AW * kH + kH];  // S rows then msum
-    const int t = threadIdx.x, h = t & (kH - 1), kq = t >> 6;
-    float dW2[16], dU1[16], dW1[NK], vec = 0.f, dc2 = 0.f, loss = 0.f;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) dW2[i] = dU1[i] = 0.f;
-#pragma unroll
-    for (int i = 0; i < NK; ++i) dW1[i] = 0.f;
-    const int64_t b0 = (int64_t)blockIdx.x * g.per_cta;
-    const int64_t b1 = min((int64_t)g.B, b0 + g.per_cta);
-    for (int64_t cb = b0; cb < b1; cb += CH) {
-        const int nq = (int)min((int64_t)CH, b1 - cb);
-        __syncthreads();
-        for (int i = t; i < nq * kVecStride; i += blockDim.x)
-            cp_async4(&wv[i / kVecStride][i % kVecStride], g.work + cb * kVecStride + i);
-        for (int i = t; i < nq * AW * kH; i += blockDim.x)
-            cp_async4(&sv[i / (AW * kH)][i % (AW * kH)], g.s + cb * AW * kH + i);
-        for (int i = t; i < nq * kH; i += blockDim.x) cp_async4(&sv[i / kH][AW * kH + i % kH], g.msum + cb * kH + i);
-        cp_async_wait_all();
-        __syncthreads();
-        for (int q = 0; q < nq; ++q) {
-            const float *w = wv[q];
-            const float dhq = w[kDHQ + h], dz2 = w[kDZ2 + h], gg = w[kG + h];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                dW2[i] = fmaf(w[kPM + kq + 4 * i], dhq, dW2[i]);
-                dU1[i] = fmaf(w[kHQ + kq + 4 * i], dz2, dU1[i]);
-            }
-#pragma unroll
-            for (int i = 0; i < NK; ++i)
-                if (kq + 4 * i < AW) dW1[i] = fmaf(sv[q][(kq + 4 * i) * kH + h], gg, dW1[i]);
-            if (kq == 0)
-                vec = fmaf(sv[q][AW * kH + h], gg, vec);  // db1
-            else if (kq == 1)
-                vec += dhq;                               // db2
-            else if (kq == 2)
-                vec += dz2;                               // dc1
-            else
-                vec += w[kA2DL + h];                      // du2
-            if (t == 0) {
-                dc2 += w[kDL];
-                loss += w[kLOSS];
-            }
-        }
-    }
-    float *row = g.partial + (int64_t)blockIdx.x * (g.off.total + 1);
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-        row[g.off.w2 + (kq + 4 * i) * kH + h] = dW2[i];
-        row[g.off.u1 + (kq + 4 * i) * kH + h] = dU1[i];
-    }
-#pragma unroll
-    for (int i = 0; i < NK; ++i)
-        if (kq + 4 * i < AW) row[g.off.w1 + (kq + 4 * i) * kH + h] = dW1[i];
-    const int vo = kq == 0 ? g.off.b1 : (kq == 1 ? g.off.b2 : (kq == 2 ? g.off.c1 : g.off.u2));
-    row[vo + h] = vec;
-    if (t == 0) {
-        row[g.off.c2] = dc2;
-        row[g.off.total] = loss / (float)g.B;
-    }
-}
 
 // Sum the per-CTA partial gradients in a fixed order and apply Adam
 // (encoder.py:236-249) with bias corrections from the device step counter.
@@ -254,6 +85,7 @@ __global__ void __launch_bounds__(kAdamCols *kAdamGroups) adam_kernel(
     __shared__ float part[kAdamGroups][kAdamCols];
     const int c = threadIdx.x & (kAdamCols - 1), grp = threadIdx.x / kAdamCols;
     const int i = blockIdx.x * kAdamCols + c;
+    pdl_wait();  // the partial rows of the tail kernel
     float gsum = 0.f;
     if (i <= n) gsum = strided_sum(partial + i, (int64_t)(n + 1), grp, rows);
     part[grp][c] = gsum;
@@ -291,13 +123,233 @@ __global__ void __launch_bounds__(kAdamCols *kAdamGroups) sum_rows_kernel(const 
     out[i] = gsum;
 }
 
+// ---------------------------------------------------------------------------
+// Tensor-core tail: one CTA (4 warps) per chunk of 16 queries.  The five
+// [16 x 64] x [64 x 64] products of the tail (hq, z2, dhq, g) and the rank-16
+// gradient updates (dW2 += pm^T dhq, dU1 += hq^T dz2) run as m16n8k8 TF32
+// MMAs in the 3-pass split (a_hi b_hi + a_hi b_lo + a_lo b_hi: fp32-level
+// accuracy); W2 / U1 are staged once per CTA in shared memory.
+constexpr int kTQ = 16;   // queries per chunk (the MMA M dimension)
+constexpr int kTP = 68;   // shared-memory row pitch (floats)
+
+__device__ __forceinline__ void tf32_split(float x, uint32_t &hi, uint32_t &lo) {
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
+    const float r = x - __uint_as_float(hi);
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lo) : "f"(r));
+}
+
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// acc[nt] += A[16 x 8KS] B[8KS x 8NT] for one warp; la(m, k) = A[m][k],
+// lb(k, nt) = B[k][8 nt + gq]
+template <int NT, int KS, class LA, class LB>
+__device__ __forceinline__ void warp_mma3(float (&acc)[NT][4], int lane, LA la, LB lb) {
+    const int gq = lane >> 2, tq = lane & 3;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+        uint32_t ah[4], al[4];
+        tf32_split(la(gq, 8 * ks + tq), ah[0], al[0]);
+        tf32_split(la(gq + 8, 8 * ks + tq), ah[1], al[1]);
+        tf32_split(la(gq, 8 * ks + tq + 4), ah[2], al[2]);
+        tf32_split(la(gq + 8, 8 * ks + tq + 4), ah[3], al[3]);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            uint32_t bh0, bl0, bh1, bl1;
+            tf32_split(lb(8 * ks + tq, nt), bh0, bl0);
+            tf32_split(lb(8 * ks + tq + 4, nt), bh1, bl1);
+            mma_tf32(acc[nt], al, bh0, bh1);
+            mma_tf32(acc[nt], ah, bl0, bl1);
+            mma_tf32(acc[nt], ah, bh0, bh1);
+        }
+    }
+}
+
+template <int AW>
+__global__ void __launch_bounds__(128) tail_tc_kernel(TailArgs g) {
+    extern __shared__ __align__(16) float tsm[];
+    float *W2s = tsm, *U1s = W2s + 64 * kTP;               // [64][kTP] row-major W2, U1
+    float *PM = U1s + 64 * kTP, *HQ = PM + kTQ * kTP, *Z2 = HQ + kTQ * kTP;
+    float *DZ2 = Z2 + kTQ * kTP, *DHQ = DZ2 + kTQ * kTP, *G = DHQ + kTQ * kTP;  // [kTQ][kTP] each
+    float *vsm = G + kTQ * kTP;                             // [4 warps][64] du2 partials | dl | loss
+    float *SS = vsm + 272;                                  // [kTQ][(AW+1)*64] S | msum of the chunk
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
+    const float *P = g.params;
+    for (int i = tid; i < 64 * 16; i += 128) {
+        const int r = i >> 4, c = (i & 15) * 4;
+        cp_async16(W2s + r * kTP + c, P + g.off.w2 + r * 64 + c);
+        cp_async16(U1s + r * kTP + c, P + g.off.u1 + r * 64 + c);
+    }
+    const float u2a = P[g.off.u2 + lane], u2b = P[g.off.u2 + lane + 32], c2 = P[g.off.c2];
+    pdl_wait();     // pooled / S / msum of the join+encode kernel
+    pdl_trigger();  // the Adam kernel may get scheduled
+    const bool train = g.labels != nullptr;
+    const int64_t q_lo = (int64_t)blockIdx.x * g.per_cta;
+    const int64_t q_hi = min(g.B, q_lo + g.per_cta);
+    constexpr int NW1 = ((AW + 1) * 64 + 127) / 128;
+    float aw2[8][4], au1[8][4], aw1[NW1], vacc = 0.f, du2a = 0.f, du2b = 0.f, dc2 = 0.f, lsum = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) aw2[i][r] = au1[i][r] = 0.f;
+#pragma unroll
+    for (int i = 0; i < NW1; ++i) aw1[i] = 0.f;
+    cp_async_wait_all();
+    __syncthreads();
+    for (int64_t q0 = q_lo; q0 < q_hi; q0 += kTQ) {
+        const int nq = (int)min((int64_t)kTQ, q_hi - q0);
+        if (train) {  // the chunk's S and msum, in flight while the products run
+            for (int i = tid; i < nq * AW * 16; i += 128) {
+                const int q = i / (AW * 16), c = i - q * AW * 16;
+                cp_async16(SS + q * (AW + 1) * 64 + c * 4, g.s + (q0 + q) * AW * 64 + c * 4);
+            }
+            for (int i = tid; i < nq * 16; i += 128)
+                cp_async16(SS + (i >> 4) * (AW + 1) * 64 + AW * 64 + (i & 15) * 4, g.msum + (q0 + (i >> 4)) * 64 + (i & 15) * 4);
+        }
+        for (int i = tid; i < kTQ * 64; i += 128) {
+            const int q = i >> 6, k = i & 63;
+            PM[q * kTP + k] = q < nq ? g.pooled[(q0 + q) * 64 + k] * g.scale : 0.f;
+        }
+        __syncthreads();
+        // hq = pm W2 + b2 ; z2 = hq U1 + c1   (warp w: output columns 16w .. 16w+15)
+#pragma unroll
+        for (int pass = 0; pass < 2; ++pass) {
+            const float *X = pass ? HQ : PM, *M = pass ? U1s : W2s, *bias = P + (pass ? g.off.c1 : g.off.b2);
+            float *Y = pass ? Z2 : HQ;
+            float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+            warp_mma3<2, 8>(acc, lane, [&](int m, int k) { return X[m * kTP + k]; },
+                            [&](int k, int nt) { return M[k * kTP + 16 * warp + 8 * nt + gq]; });
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+                const int c = 16 * warp + 8 * nt + 2 * tq;
+                Y[gq * kTP + c] = acc[nt][0] + bias[c];
+                Y[gq * kTP + c + 1] = acc[nt][1] + bias[c + 1];
+                Y[(gq + 8) * kTP + c] = acc[nt][2] + bias[c];
+                Y[(gq + 8) * kTP + c + 1] = acc[nt][3] + bias[c + 1];
+            }
+            __syncthreads();
+        }
+        // logits, BCE and dz2 (warp w: queries w, w+4, w+8, w+12)
+        for (int q = warp; q < kTQ; q += 4) {
+            const float za = Z2[q * kTP + lane], zb = Z2[q * kTP + lane + 32];
+            float part = fmaxf(za, 0.f) * u2a + fmaxf(zb, 0.f) * u2b;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
+            const float z = part + c2;
+            float dl = 0.f;
+            if (q < nq) {
+                if (g.logits && lane == 0) g.logits[q0 + q] = z;
+                if (train) {
+                    const float y = g.labels[q0 + q];
+                    const float sig = z >= 0.f ? 1.f / (1.f + expf(-z)) : expf(z) / (1.f + expf(z));
+                    dl = (sig - y) * g.inv_b;
+                    if (lane == 0) {
+                        dc2 += dl;
+                        lsum += fmaxf(z, 0.f) - z * y + log1pf(expf(-fabsf(z)));
+                    }
+                    du2a = fmaf(fmaxf(za, 0.f), dl, du2a);
+                    du2b = fmaf(fmaxf(zb, 0.f), dl, du2b);
+                }
+            }
+            DZ2[q * kTP + lane] = za > 0.f ? dl * u2a : 0.f;
+            DZ2[q * kTP + lane + 32] = zb > 0.f ? dl * u2b : 0.f;
+        }
+        __syncthreads();
+        if (!train) continue;
+        // dhq[q][k] = sum_h dz2[q][h] U1[k][h] ; g[q][k] = scale sum_h dhq[q][h] W2[k][h]
+#pragma unroll
+        for (int pass = 0; pass < 2; ++pass) {
+            const float *X = pass ? DHQ : DZ2, *M = pass ? W2s : U1s;
+            float *Y = pass ? G : DHQ;
+            const float mul = pass ? g.scale : 1.f;
+            float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+            warp_mma3<2, 8>(acc, lane, [&](int m, int k) { return X[m * kTP + k]; },
+                            [&](int k, int nt) { return M[(16 * warp + 8 * nt + gq) * kTP + k]; });
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+                const int c = 16 * warp + 8 * nt + 2 * tq;
+                Y[gq * kTP + c] = acc[nt][0] * mul;
+                Y[gq * kTP + c + 1] = acc[nt][1] * mul;
+                Y[(gq + 8) * kTP + c] = acc[nt][2] * mul;
+                Y[(gq + 8) * kTP + c + 1] = acc[nt][3] * mul;
+            }
+            __syncthreads();
+        }
+        // dW2 += pm^T dhq, dU1 += hq^T dz2  (warp w: rows 16w .. 16w+15, all 64 columns)
+        warp_mma3<8, 2>(aw2, lane, [&](int m, int k) { return PM[k * kTP + 16 * warp + m]; },
+                        [&](int k, int nt) { return DHQ[k * kTP + 8 * nt + gq]; });
+        warp_mma3<8, 2>(au1, lane, [&](int m, int k) { return HQ[k * kTP + 16 * warp + m]; },
+                        [&](int k, int nt) { return DZ2[k * kTP + 8 * nt + gq]; });
+        // dW1[c][h] += S_q[c][h] g_q[h], db1[h] += msum_q[h] g_q[h]; db2 = sum dhq, dc1 = sum dz2
+        cp_async_wait_all();
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < NW1; ++i) {
+            const int e = tid + 128 * i;
+            if (e < (AW + 1) * 64) {
+                float a = aw1[i];
+                for (int q = 0; q < nq; ++q) a = fmaf(SS[q * (AW + 1) * 64 + e], G[q * kTP + (e & 63)], a);
+                aw1[i] = a;
+            }
+        }
+        {
+            const float *V = tid < 64 ? DHQ : DZ2;
+            for (int q = 0; q < nq; ++q) vacc += V[q * kTP + (tid & 63)];
+        }
+        __syncthreads();
+    }
+    if (g.step_inc && blockIdx.x == 0 && tid == 0) *g.step_inc += 1;
+    if (!train) return;
+    // ---- partial row of this CTA: [grads | loss]
+    float *row = g.partial + (int64_t)blockIdx.x * (g.off.total + 1);
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+        const int r0 = 16 * warp + gq, c = 8 * nt + 2 * tq;
+        row[g.off.w2 + r0 * 64 + c] = aw2[nt][0];
+        row[g.off.w2 + r0 * 64 + c + 1] = aw2[nt][1];
+        row[g.off.w2 + (r0 + 8) * 64 + c] = aw2[nt][2];
+        row[g.off.w2 + (r0 + 8) * 64 + c + 1] = aw2[nt][3];
+        row[g.off.u1 + r0 * 64 + c] = au1[nt][0];
+        row[g.off.u1 + r0 * 64 + c + 1] = au1[nt][1];
+        row[g.off.u1 + (r0 + 8) * 64 + c] = au1[nt][2];
+        row[g.off.u1 + (r0 + 8) * 64 + c + 1] = au1[nt][3];
+    }
+#pragma unroll
+    for (int i = 0; i < NW1; ++i) {
+        const int e = tid + 128 * i;
+        if (e < AW * 64)
+            row[g.off.w1 + e] = aw1[i];
+        else if (e < (AW + 1) * 64)
+            row[g.off.b1 + e - AW * 64] = aw1[i];
+    }
+    row[(tid < 64 ? g.off.b2 : g.off.c1) + (tid & 63)] = vacc;
+    vsm[warp * 64 + lane] = du2a;
+    vsm[warp * 64 + lane + 32] = du2b;
+    if (lane == 0) {
+        vsm[256 + warp] = dc2;
+        vsm[260 + warp] = lsum;
+    }
+    __syncthreads();
+    if (tid < 64) row[g.off.u2 + tid] = (vsm[tid] + vsm[64 + tid]) + (vsm[128 + tid] + vsm[192 + tid]);
+    if (tid == 64) row[g.off.c2] = (vsm[256] + vsm[257]) + (vsm[258] + vsm[259]);
+    if (tid == 65) row[g.off.total] = ((vsm[260] + vsm[261]) + (vsm[262] + vsm[263])) * g.inv_b;
+}
+
+template <int AW>
+constexpr size_t tail_smem() { return (size_t)(2 * 64 * kTP + 6 * kTQ * kTP + 272 + kTQ * (AW + 1) * 64) * 4; }
+
 using TailKernel = void (*)(TailArgs);
 
-static TailKernel pick_tail(int aw) {
+static TailKernel pick_tail(int aw, size_t &smem) {
     switch (aw) {
 #define WJ_T(x) \
-    case x: return tail_grad_kernel<x>;
-        WJ_T(2) WJ_T(3) WJ_T(4) WJ_T(5) WJ_T(6) WJ_T(8) WJ_T(9) WJ_T(10) WJ_T(12) WJ_T(14) WJ_T(15)
+    case x: smem = tail_smem<x>(); return tail_tc_kernel<x>;
+        WJ_T(2) WJ_T(3) WJ_T(4) WJ_T(5) WJ_T(6) WJ_T(7) WJ_T(8) WJ_T(9) WJ_T(10) WJ_T(12) WJ_T(14) WJ_T(15)
         WJ_T(16)
 #undef WJ_T
         default: return nullptr;
@@ -310,22 +362,24 @@ extern "C" int wj_encoder_tail(const float *pooled, const float *s, const float 
                                const float *labels, int64_t n_batch, int32_t aw, int32_t hidden,
                                const float *params, const int32_t *offsets9, float scale,
                                float *logits_out, float *partial, int32_t partial_rows, float *work,
-                               wj_stream_t stream) {
+                               int64_t *step_inc, wj_stream_t stream) {
     using namespace wj;
     if (hidden != kH) {
         set_error("encoder tail kernel supports hidden=64 (got %d)", hidden);
         return WJ_ERR_UNSUPPORTED;
     }
-    TailKernel k = pick_tail(aw);
+    size_t smem = 0;
+    TailKernel k = pick_tail(aw, smem);
     if (!k) {
         set_error("encoder tail not instantiated for A*(L+1)=%d", aw);
         return WJ_ERR_UNSUPPORTED;
     }
-    if (labels && (!s || !msum || !partial || !work || partial_rows < 1)) {
-        set_error("training tail needs S, msum, a partial buffer and a work buffer");
+    if (labels && (!s || !msum || !partial || partial_rows < 1)) {
+        set_error("training tail needs S, msum and a partial buffer");
         return WJ_ERR_ARG;
     }
-    if (n_batch == 0) return WJ_OK;
+    (void)work;  // not needed by the tensor-core tail (kept for ABI stability)
+    if (n_batch == 0 && !labels) return WJ_OK;
     TailArgs g;
     g.pooled = pooled;
     g.s = s;
@@ -336,16 +390,26 @@ extern "C" int wj_encoder_tail(const float *pooled, const float *s, const float 
     g.off = {offsets9[0], offsets9[1], offsets9[2], offsets9[3], offsets9[4],
              offsets9[5], offsets9[6], offsets9[7], offsets9[8]};
     g.scale = scale;
+    g.inv_b = n_batch > 0 ? 1.f / (float)n_batch : 0.f;
     g.logits = logits_out;
     g.partial = partial;
-    g.work = work;
-    g.per_cta = (int)((n_batch + partial_rows - 1) / partial_rows);
-    const int64_t groups = (n_batch + kTailWarps - 1) / kTailWarps;
-    const int64_t grid = groups < 4096 ? groups : 4096;
-    tail_vec_kernel<<<(unsigned)grid, kTailWarps * 32, 0, (cudaStream_t)stream>>>(g);
-    if (!labels) return check_launch("wj_encoder_tail");
-    // exactly partial_rows CTAs: rows past the last query write zeros
-    k<<<(unsigned)partial_rows, 256, 0, (cudaStream_t)stream>>>(g);
+    g.work = nullptr;
+    g.step_inc = step_inc;
+    // training: exactly partial_rows CTAs, CTA i owns queries [i*q, (i+1)*q),
+    // q = ceil(B / partial_rows) (rows past the last query are zeros);
+    // inference: one CTA per 16 queries
+    const int64_t rows = labels ? partial_rows : (n_batch + kTQ - 1) / kTQ;
+    g.per_cta = (int)((n_batch + rows - 1) / rows);
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) {
+        set_error("tail smem attribute: %s", cudaGetErrorString(e));
+        return WJ_ERR_CUDA;
+    }
+    e = launch_pdl(k, dim3((unsigned)rows), dim3(128), smem, (cudaStream_t)stream, g);
+    if (e != cudaSuccess) {
+        set_error("wj_encoder_tail launch: %s", cudaGetErrorString(e));
+        return WJ_ERR_CUDA;
+    }
     return check_launch("wj_encoder_tail");
 }
 
@@ -359,8 +423,13 @@ extern "C" int wj_adam(float *params, float *m, float *v, const float *partial,
         return WJ_ERR_ARG;
     }
     const int blocks = (n_params + 1 + kAdamCols - 1) / kAdamCols;
-    adam_kernel<<<blocks, kAdamCols * kAdamGroups, 0, (cudaStream_t)stream>>>(
-        params, m, v, partial, partial_rows, n_params, lr, beta1, beta2, eps, step, grad_out, loss_out);
+    const cudaError_t e = launch_pdl(adam_kernel, dim3(blocks), dim3(kAdamCols * kAdamGroups), 0, (cudaStream_t)stream,
+                                     params, m, v, partial, partial_rows, n_params, lr, beta1, beta2, eps, step,
+                                     grad_out, loss_out);
+    if (e != cudaSuccess) {
+        set_error("wj_adam launch: %s", cudaGetErrorString(e));
+        return WJ_ERR_CUDA;
+    }
     return check_launch("wj_adam");
 }
 

@@ -257,8 +257,7 @@ class TrainStep:
                 return {"pooled": torch.empty((B, H), device=self.dev),
                         "S": torch.empty((B, AW, H), device=self.dev),
                         "msum": torch.empty((B, H), device=self.dev),
-                        "work": torch.empty((B, 6 * H + 8), device=self.dev),
-                        "partial": torch.empty((rows, int(self.offs[-1]) + 1), device=self.dev)}
+                            "partial": torch.empty((rows, int(self.offs[-1]) + 1), device=self.dev)}
             H, AW = self.params.hidden, A * self.store.width
             return {"pooled": torch.empty((B, H), device=self.dev),
                     "S": torch.empty((B, AW, H), device=self.dev),
@@ -273,7 +272,6 @@ class TrainStep:
 
         p, st, store = self.params, self.state, self.store
         B, A = q.shape
-        self.step_t.add_(1)
         keep = (1.0 - p.dropout) if p.dropout > 0.0 else 1.0
         scale = 1.0 / (keep * A * store.landings)
         dev = _lib.stream_handle(self.dev)
@@ -281,7 +279,7 @@ class TrainStep:
         E.forward_fused(p, store, q, training=True, seed=self.seed, step=self.step_t, out=bufs, tail=False)
         _lib.call("wj_encoder_tail", _lib.ptr(bufs["pooled"]), _lib.ptr(bufs["S"]), _lib.ptr(bufs["msum"]),
                   _lib.ptr(y), B, A * store.width, p.hidden, _lib.ptr(self.flat), self.offs_c, scale,
-                  None, _lib.ptr(bufs["partial"]), rows, _lib.ptr(bufs["work"]), dev)
+                  None, _lib.ptr(bufs["partial"]), rows, None, _lib.ptr(self.step_t), dev)
         partial, prow = bufs["partial"], rows
         if self.group is not None:
             from .distributed import all_reduce_mean
@@ -298,11 +296,14 @@ class TrainStep:
     def _body(self, q, y, bufs, inv_bc):
         if self.fast_tail:
             return self._fast_body(q, y, bufs)
-        self.step_t.add_(1)
         if self.mode == "fused":
+            # the dropout stream is keyed by the step counter BEFORE this step's
+            # increment (the fast path's tail kernel increments it)
             logits, cache = E.forward_fused(self.params, self.store, q, training=True, seed=self.seed,
                                             step=self.step_t, out=bufs)
+            self.step_t.add_(1)
         else:
+            self.step_t.add_(1)
             dense_batch(self.store, q, dtype=self.dense_dtype, out=bufs["dense"], validate=False,
                         features=self.features)
             logits, cache = E.forward(self.params, bufs["dense"], training=True, mode=self.mode)
@@ -320,7 +321,8 @@ class TrainStep:
         t = self.state.step
         self._host_bc[0] = 1.0 / (1.0 - self.state.beta1 ** t)
         self._host_bc[1] = 1.0 / (1.0 - self.state.beta2 ** t)
-        self.inv_bc.copy_(self._host_bc, non_blocking=True)
+        if not self.fast_tail:  # the kernel path derives the corrections from the device step counter
+            self.inv_bc.copy_(self._host_bc, non_blocking=True)
 
     def __call__(self, q: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
         """q: [B, A] int64 ids, y: [B] labels (device, or pinned host for the
