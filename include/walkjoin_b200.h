@@ -119,7 +119,9 @@ int wj_join(const int64_t *queries, int64_t n_batch, int32_t arity, const int32_
  * joined RPE row of walk slot r and d_r a Bernoulli(keep_prob) dropout draw
  * from a counter-based stream keyed by (seed, *step, b, virtual landing,
  * unit) (keep_prob = 1: no dropout).  *step is read on the device so a
- * captured CUDA graph advances it itself.  voff / vcnt / vslots are the
+ * captured CUDA graph advances it itself.  cross (nullable) holds the
+ * query's cross RPE ids computed by wj_join_cross; then the kernel does no
+ * searches, while NULL makes it search the sorted lists itself.  voff / vcnt / vslots are the
  * store's virtual-landing index (wj_vindex_count / wj_vindex_fill) and
  * table_rows_f16 the fp16 table rows (wj_table_rows_f16); with them,
  * hidden = 64, A*(L+1) <= 15, L+1 <= 8 and M <= 2048 run the tensor-core
@@ -128,12 +130,22 @@ int wj_join(const int64_t *queries, int64_t n_batch, int32_t arity, const int32_
  * pipeline._dense_batch + the first layer of encoder.forward/backward
  * (_kernels.py:209-245, pipeline.py:169-182, encoder.py:150-161,224-232). */
 int wj_join_encode(const int64_t *queries, int64_t n_batch, int32_t arity, const int64_t *offsets,
-                   const int32_t *uniq_x, const int32_t *uniq_id, const int64_t *voff,
+                   const int32_t *uniq_x, const int32_t *uniq_id, const int32_t *cross, const int64_t *voff,
                    const int32_t *vcnt, const uint16_t *vslots, const uint16_t *table_rows_f16,
                    int32_t num_walks, int32_t num_steps, int32_t max_unique,
                    const uint64_t *table_keys, int64_t table_len, const float *w1, const float *b1,
                    int32_t hidden, float keep_prob, uint64_t seed, const int64_t *step,
                    float *pooled_out, float *s_out, float *msum_out, wj_stream_t stream);
+
+/* Cross RPE ids of every distinct landing of every query anchor:
+ * cross_out [B, A, A-1, max_unique] int32, entry [b, a, jj, l] = RPE id of
+ * the l-th landing (sorted order) of anchor a relative to the jj-th other
+ * anchor of query b, 0 if absent; entries l >= U_a are left untouched.  The
+ * per-landing form of the rpe_ids columns _kernels.join_fill writes per walk
+ * slot (_kernels.py:237-245).  A in {2, 3}. */
+int wj_join_cross(const int64_t *queries, int64_t n_batch, int32_t arity, const int64_t *offsets,
+                  const int32_t *uniq_x, const int32_t *uniq_id, int32_t max_unique, int32_t *cross_out,
+                  wj_stream_t stream);
 
 /* Virtual-landing index of a store (the encoder input layout; no reference
  * counterpart -- it describes the rows pipeline._dense_batch builds,

@@ -65,7 +65,7 @@ struct EncMmaArgs {
     const uint16_t *vslots;
     const uint4 *trow;  // [tlen] fp16 count rows (8 halves)
     int mu, lcap, xr_bytes;
-    int lstep;  // largest power of two <= mu (binary-search stride)
+    const int32_t *cross;  // [B][A][A-1][mu] cross RPE ids (wj_join_cross) or null: search in-kernel
     const float *w1;  // [AW, 64]
     const float *b1;  // [64]
     uint32_t t11, t21, t22;  // packed 14-bit thresholds (both lanes): 1-row; 2-row K>=1, K>=2
@@ -111,28 +111,6 @@ __device__ __forceinline__ uint32_t hadd2_u32(uint32_t a, uint32_t b) {
     uint32_t r;
     asm("add.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
     return r;
-}
-
-// a[i] for a runtime i < A without dynamic register indexing
-template <int A>
-__device__ __forceinline__ int pick(const int (&a)[A], int i) {
-    int v = a[0];
-#pragma unroll
-    for (int k = 1; k < A; ++k)
-        if (i == k) v = a[k];
-    return v;
-}
-
-__device__ __forceinline__ int lb_i32(const int32_t *a, int n, int32_t x) {
-    int lo = 0, hi = n;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (a[mid] < x)
-            lo = mid + 1;
-        else
-            hi = mid;
-    }
-    return lo;
 }
 
 // Output word k of the row [x | 1 | 0...] (16 fp16 columns), where column
@@ -216,6 +194,99 @@ __device__ __forceinline__ void tile(const uint16_t *lst, uint32_t xr_s, uint32_
     }
 }
 
+// Cross RPE ids by merging the anchors' sorted lists (merge path): for every
+// anchor pair (a, j) thread tid of nthr takes an equal slice of the merged
+// order (one diagonal binary search, then a linear merge); equal ids are
+// emitted list-a first, so an element of list j finds its partner at list a's
+// previous position.  scr[a][jj][l] = RPE id of landing l of anchor a relative
+// to the jj-th other anchor (0 if absent).
+template <int A>
+__device__ __forceinline__ void merge_cross(int tid, int nthr, int mu, const int32_t *sx, const int32_t *sid,
+                                            const int (&U)[A], int32_t *scr) {
+#pragma unroll
+    for (int a = 0; a < A; ++a)
+#pragma unroll
+        for (int j = a + 1; j < A; ++j) {
+            const int n0 = U[a], n1 = U[j], tot = n0 + n1;
+            const int32_t *X0 = sx + a * mu, *X1 = sx + j * mu, *I0 = sid + a * mu, *I1 = sid + j * mu;
+            int32_t *o0 = scr + (a * (A - 1) + (j - 1)) * mu;  // list a relative to j (jj = j - 1: j > a)
+            int32_t *o1 = scr + (j * (A - 1) + a) * mu;        // list j relative to a (jj = a: a < j)
+            const int d0 = (tid * tot) / nthr, d1 = ((tid + 1) * tot) / nthr;
+            int lo = max(0, d0 - n1), hi = min(d0, n0);
+            while (lo < hi) {  // merge-path split of diagonal d0 (ties: list a first)
+                const int mid = (lo + hi) >> 1;
+                if (X0[mid] <= X1[d0 - mid - 1])
+                    lo = mid + 1;
+                else
+                    hi = mid;
+            }
+            int i0 = lo, i1 = d0 - lo;
+            int32_t x0 = i0 < n0 ? X0[i0] : INT32_MAX, x1 = i1 < n1 ? X1[i1] : INT32_MAX;
+            for (int d = d0; d < d1; ++d) {
+                if (x0 <= x1 && i0 < n0) {
+                    o0[i0] = x0 == x1 ? I1[i1] : 0;
+                    ++i0;
+                    x0 = i0 < n0 ? X0[i0] : INT32_MAX;
+                } else {
+                    o1[i1] = (i0 > 0 && X0[i0 - 1] == x1) ? I0[i0 - 1] : 0;
+                    ++i1;
+                    x1 = i1 < n1 ? X1[i1] : INT32_MAX;
+                }
+            }
+        }
+}
+
+// Row build from precomputed cross ids (wj_join_cross): no searches, the
+// fp16 table rows of kRowU landings are loaded together.
+template <int A, int W>
+__device__ __forceinline__ void build_rows_x(const EncMmaArgs &g, int tid, int nthr, const int32_t *scr,
+                                             const int32_t *sid, const int (&pu)[A + 1], unsigned char *xr) {
+    const int mu = g.mu;
+    const int LT = pu[A];
+    for (int e0 = tid; e0 < LT; e0 += kRowU * nthr) {
+        uint4 t4[kRowU][A];
+        int rowi[kRowU];
+#pragma unroll
+        for (int u = 0; u < kRowU; ++u) {
+            const int e = e0 + u * nthr;
+            const bool ok = e < LT;
+            int a = 0;
+#pragma unroll
+            for (int t = 1; t < A; ++t) a += e >= pu[t];
+            int base_a = 0;
+#pragma unroll
+            for (int t = 1; t < A; ++t)
+                if (a == t) base_a = pu[t];
+            const int l = ok ? e - base_a : 0;
+            rowi[u] = ok ? a * mu + l : -1;
+#pragma unroll
+            for (int j = 0; j < A; ++j) {
+                const int jj = j < a ? j : j - 1;
+                const int id = !ok ? 0 : (j == a ? sid[a * mu + l] : scr[(a * (A - 1) + jj) * mu + l]);
+                t4[u][j] = __ldg(g.trow + id);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kRowU; ++u) {
+            if (rowi[u] < 0) continue;
+            uint32_t r[A][4];
+#pragma unroll
+            for (int j = 0; j < A; ++j) {
+                r[j][0] = t4[u][j].x;
+                r[j][1] = t4[u][j].y;
+                r[j][2] = t4[u][j].z;
+                r[j][3] = t4[u][j].w;
+            }
+            uint32_t w[8];
+            splice_row<A, W>(r, w);
+            const uint32_t row = (uint32_t)rowi[u];
+            const uint32_t sw = (row >> 2) & 1u;
+            *reinterpret_cast<uint4 *>(xr + row * kRowB + (sw << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+            *reinterpret_cast<uint4 *>(xr + row * kRowB + ((sw ^ 1u) << 4)) = make_uint4(w[4], w[5], w[6], w[7]);
+        }
+    }
+}
+
 template <int A, int AW, int kMW, int MINB>
 __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaArgs g) {
     static_assert(AW + 1 <= 16, "one k16 step: A*(L+1) + 1 <= 16");
@@ -234,9 +305,10 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
     float *wscale = reinterpret_cast<float *>(meta + kMetaQ * 3);       // [2]
     unsigned char *xr = smem_raw + kWtBytes + kHdrBytes;                // rows [A*mu + 1][32 B] | red
     float *red = reinterpret_cast<float *>(xr);                         // [warps][64][kRedS] (after tiles)
-    int32_t *sx = reinterpret_cast<int32_t *>(xr + g.xr_bytes);         // [A][mu]
-    int32_t *sid = sx + A * mu;                                         // [A][mu]
-    uint16_t *vl = reinterpret_cast<uint16_t *>(sid + A * mu);          // [lcap] virtual landing rows
+    int32_t *sx = reinterpret_cast<int32_t *>(xr + g.xr_bytes);         // [A][mu] sorted landing lists
+    int32_t *sid = sx + A * mu;                                         // [A][mu] their RPE ids
+    int32_t *scr = sid + A * mu;                                        // [A][A-1][mu] cross RPE ids
+    uint16_t *vl = reinterpret_cast<uint16_t *>(scr + A * (A - 1) * mu);  // [lcap] virtual landing rows
     const uint32_t xr_s = smem_u32(xr), wt_s = smem_u32(wt);
     const uint32_t zrow = (uint32_t)(A * mu);  // all-zero row: padding (contributes nothing)
 
@@ -318,9 +390,15 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
             const int32_t *gx = g.ux + qm[a].lo;
             const int32_t *gi = g.uid + qm[a].lo;
             for (int i = threadIdx.x; i < U[a]; i += NT) {
-                cp_async4(sx + a * mu + i, gx + i);
+                if (!g.cross) cp_async4(sx + a * mu + i, gx + i);
                 cp_async4(sid + a * mu + i, gi + i);
             }
+            if (g.cross)
+#pragma unroll
+                for (int jj = 0; jj < A - 1; ++jj) {
+                    const int32_t *gc = g.cross + (b * A * (A - 1) + a * (A - 1) + jj) * (int64_t)mu;
+                    for (int i = threadIdx.x; i < U[a]; i += NT) cp_async4(scr + (a * (A - 1) + jj) * mu + i, gc + i);
+                }
         }
 #pragma unroll
         for (int a = 0; a < A; ++a) {
@@ -335,86 +413,11 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
         cp_async_wait_all();
         __syncthreads();
 
-        // ---- one fp16 row per distinct landing.  Thread t owns landings
-        // e = t, t + NT, ... of the concatenated lists; the RPE id of landing
-        // x relative to anchor j != a is a fixed-step (branch-free) binary
-        // search of x in j's sorted list, kRowU landings at a time so the
-        // searches and the fp16 table-row loads overlap
-        {
-            const int LT = pu[A];
-            for (int e0 = threadIdx.x; e0 < LT; e0 += kRowU * NT) {
-                int ids[kRowU][A], rowi[kRowU], la[kRowU], xs[kRowU], own[kRowU], pos[kRowU][A];
-#pragma unroll
-                for (int u = 0; u < kRowU; ++u) {
-                    const int e = e0 + u * NT;
-                    const bool ok = e < LT;
-                    int a = 0;
-#pragma unroll
-                    for (int t = 1; t < A; ++t) a += e >= pu[t];
-                    int base_a = 0;
-#pragma unroll
-                    for (int t = 1; t < A; ++t)
-                        if (a == t) base_a = pu[t];
-                    const int l = ok ? e - base_a : 0;
-                    la[u] = a;
-                    rowi[u] = ok ? a * mu + l : -1;
-                    xs[u] = sx[a * mu + l];
-                    own[u] = sid[a * mu + l];
-#pragma unroll
-                    for (int jj = 0; jj < A; ++jj) pos[u][jj] = 0;
-                }
-                // searches of x in the other anchors' lists, all (u, j) in lock step
-#pragma unroll
-                for (int sh = 15; sh >= 0; --sh) {
-                    const int step = 1 << sh;
-                    if (step > g.lstep) continue;
-#pragma unroll
-                    for (int u = 0; u < kRowU; ++u)
-#pragma unroll
-                        for (int jj = 0; jj < A - 1; ++jj) {
-                            const int j = jj < la[u] ? jj : jj + 1;
-                            const int p = pos[u][jj] + step;
-                            if (p <= pick<A>(U, j) && sx[j * mu + p - 1] < xs[u]) pos[u][jj] = p;
-                        }
-                }
-#pragma unroll
-                for (int u = 0; u < kRowU; ++u)
-#pragma unroll
-                    for (int j = 0; j < A; ++j) {
-                        const int jj = j < la[u] ? j : j - 1;
-                        int pp = 0;
-#pragma unroll
-                        for (int k = 0; k < A - 1; ++k)
-                            if (k == jj) pp = pos[u][k];
-                        const int pc = min(pp, mu - 1);
-                        const int cross = (pp < U[j] && sx[j * mu + pc] == xs[u]) ? sid[j * mu + pc] : 0;
-                        ids[u][j] = j == la[u] ? own[u] : cross;
-                    }
-                uint4 t4[kRowU][A];
-#pragma unroll
-                for (int u = 0; u < kRowU; ++u)
-#pragma unroll
-                    for (int j = 0; j < A; ++j) t4[u][j] = __ldg(g.trow + (rowi[u] >= 0 ? ids[u][j] : 0));
-#pragma unroll
-                for (int u = 0; u < kRowU; ++u) {
-                    if (rowi[u] < 0) continue;
-                    uint32_t r[A][4];
-#pragma unroll
-                    for (int j = 0; j < A; ++j) {
-                        r[j][0] = t4[u][j].x;
-                        r[j][1] = t4[u][j].y;
-                        r[j][2] = t4[u][j].z;
-                        r[j][3] = t4[u][j].w;
-                    }
-                    uint32_t w[8];
-                    splice_row<A, W>(r, w);
-                    const uint32_t row = (uint32_t)rowi[u];
-                    const uint32_t sw = (row >> 2) & 1u;
-                    *reinterpret_cast<uint4 *>(xr + row * kRowB + (sw << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
-                    *reinterpret_cast<uint4 *>(xr + row * kRowB + ((sw ^ 1u) << 4)) = make_uint4(w[4], w[5], w[6], w[7]);
-                }
-            }
+        if (!g.cross && A > 1) {  // cross ids by merging the sorted lists
+            merge_cross<A>(threadIdx.x, NT, mu, sx, sid, U, scr);
+            __syncthreads();
         }
+        build_rows_x<A, W>(g, threadIdx.x, NT, scr, sid, pu, xr);
         __syncthreads();
 
         // ---- per-warp tiles of 16 virtual landings
@@ -478,6 +481,81 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
     }
 }
 
+// ---------------------------------------------------------------------------
+// Query-level cross RPE ids (the rpe_ids columns of _kernels.join_fill,
+// _kernels.py:237-245, per distinct landing instead of per walk slot):
+// cross[b][a][jj][l] = RPE id of landing l of anchor a relative to the jj-th
+// other anchor of query b (0 if that anchor's walks never reach it).  One
+// CTA per query stages the anchors' sorted lists in shared memory and, for
+// every anchor pair, merges the two lists (merge path: one diagonal binary
+// search per thread, then a linear merge of ~(U_a + U_j) / 128 elements);
+// equal ids are emitted list-a first, so an element of list j finds its
+// partner at list a's previous position.
+template <int A>
+__global__ void __launch_bounds__(128) join_cross_kernel(const int64_t *__restrict__ queries, int64_t n_batch,
+                                                         const int64_t *__restrict__ offsets,
+                                                         const int32_t *__restrict__ ux,
+                                                         const int32_t *__restrict__ uid, int mu,
+                                                         int32_t *__restrict__ cross) {
+    extern __shared__ __align__(16) int32_t csm[];
+    int32_t *sx = csm, *sid = csm + A * mu;
+    __shared__ int64_t lo_s[A];
+    __shared__ int un_s[A];
+    const int64_t b = blockIdx.x;
+    pdl_wait();
+    if (threadIdx.x < A) {
+        const int64_t q = queries[b * A + threadIdx.x];
+        const int64_t lo = offsets[q];
+        lo_s[threadIdx.x] = lo;
+        un_s[threadIdx.x] = (int)(offsets[q + 1] - lo);
+    }
+    __syncthreads();
+    int U[A];
+#pragma unroll
+    for (int a = 0; a < A; ++a) {
+        U[a] = un_s[a];
+        for (int i = threadIdx.x; i < U[a]; i += blockDim.x) {
+            cp_async4(sx + a * mu + i, ux + lo_s[a] + i);
+            cp_async4(sid + a * mu + i, uid + lo_s[a] + i);
+        }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    pdl_trigger();
+    int32_t *out = cross + b * (int64_t)A * (A - 1) * mu;
+#pragma unroll
+    for (int a = 0; a < A; ++a)
+#pragma unroll
+        for (int j = a + 1; j < A; ++j) {
+            const int n0 = U[a], n1 = U[j], tot = n0 + n1;
+            const int32_t *X0 = sx + a * mu, *X1 = sx + j * mu, *I0 = sid + a * mu, *I1 = sid + j * mu;
+            int32_t *o0 = out + (a * (A - 1) + (j - 1)) * mu;  // list a relative to j (jj = j - 1 since j > a)
+            int32_t *o1 = out + (j * (A - 1) + a) * mu;        // list j relative to a (jj = a since a < j)
+            const int d0 = (int)(((int64_t)threadIdx.x * tot) / blockDim.x);
+            const int d1 = (int)(((int64_t)(threadIdx.x + 1) * tot) / blockDim.x);
+            int lo = max(0, d0 - n1), hi = min(d0, n0);
+            while (lo < hi) {  // merge-path split of diagonal d0 (ties: list a first)
+                const int mid = (lo + hi) >> 1;
+                if (X0[mid] <= X1[d0 - mid - 1])
+                    lo = mid + 1;
+                else
+                    hi = mid;
+            }
+            int i0 = lo, i1 = d0 - lo;
+            for (int d = d0; d < d1; ++d) {
+                const int32_t x0 = i0 < n0 ? X0[i0] : INT32_MAX;
+                const int32_t x1 = i1 < n1 ? X1[i1] : INT32_MAX;
+                if (i0 < n0 && x0 <= x1) {
+                    o0[i0] = x0 == x1 ? I1[i1] : 0;
+                    ++i0;
+                } else {
+                    o1[i1] = (i0 > 0 && X0[i0 - 1] == x1) ? I0[i0 - 1] : 0;
+                    ++i1;
+                }
+            }
+        }
+}
+
 using EncMmaKernel = void (*)(EncMmaArgs);
 
 template <int NW, int MINB>
@@ -529,6 +607,7 @@ struct MmaPlan {
     int lcap = 0, xr_bytes = 0, mu = 1;
 };
 
+
 static int plan_mma(int arity, int num_walks, int num_steps, int max_unique, MmaPlan &pl) {
     const int W = num_steps + 1;
     // CTA shape: warps x min resident CTAs per SM (register budget); tuning
@@ -553,7 +632,8 @@ static int plan_mma(int arity, int num_walks, int num_steps, int max_unique, Mma
     const int64_t rows_b = ((int64_t)arity * pl.mu + 1) * kRowB;
     const int64_t red_b = (int64_t)pl.nw * 64 * kRedS * 4;
     pl.xr_bytes = (int)(((rows_b > red_b ? rows_b : red_b) + 15) & ~15LL);
-    pl.smem = (size_t)kWtBytes + kHdrBytes + (size_t)pl.xr_bytes + (size_t)arity * pl.mu * 8 + (size_t)pl.lcap * 2;
+    pl.smem = (size_t)kWtBytes + kHdrBytes + (size_t)pl.xr_bytes + (size_t)(2 * arity + arity * (arity - 1)) * pl.mu * 4 +
+              (size_t)pl.lcap * 2;
     if (pl.smem > 200 * 1024) {
         set_error("join_encode needs %zu B of shared memory", pl.smem);
         pl.k = nullptr;
@@ -586,8 +666,6 @@ static void fill_args(EncMmaArgs &g, const MmaPlan &pl, const int64_t *queries, 
     g.vslots = vslots;
     g.trow = reinterpret_cast<const uint4 *>(table_rows_f16);
     g.mu = pl.mu;
-    g.lstep = 1;
-    while (g.lstep * 2 <= pl.mu) g.lstep *= 2;
     g.lcap = pl.lcap;
     g.xr_bytes = pl.xr_bytes;
     binomial_thresholds14(keep_prob, g.t11, g.t21, g.t22);
@@ -599,7 +677,7 @@ static void fill_args(EncMmaArgs &g, const MmaPlan &pl, const int64_t *queries, 
 
 extern "C" int wj_join_encode(const int64_t *queries, int64_t n_batch, int32_t arity,
                               const int64_t *offsets, const int32_t *uniq_x,
-                              const int32_t *uniq_id, const int64_t *voff, const int32_t *vcnt,
+                              const int32_t *uniq_id, const int32_t *cross, const int64_t *voff, const int32_t *vcnt,
                               const uint16_t *vslots, const uint16_t *table_rows_f16,
                               int32_t num_walks, int32_t num_steps,
                               int32_t max_unique, const uint64_t *table_keys, int64_t table_len,
@@ -629,6 +707,7 @@ extern "C" int wj_join_encode(const int64_t *queries, int64_t n_batch, int32_t a
               seed, step);
     g.w1 = w1;
     g.b1 = b1;
+    g.cross = arity > 1 ? cross : nullptr;
     g.pooled = pooled_out;
     g.s_out = s_out;
     g.msum = msum_out;
@@ -643,3 +722,34 @@ extern "C" int wj_join_encode(const int64_t *queries, int64_t n_batch, int32_t a
     return check_launch("wj_join_encode");
 }
 
+
+extern "C" int wj_join_cross(const int64_t *queries, int64_t n_batch, int32_t arity, const int64_t *offsets,
+                             const int32_t *uniq_x, const int32_t *uniq_id, int32_t max_unique, int32_t *cross_out,
+                             wj_stream_t stream) {
+    using namespace wj;
+    if (arity < 2 || arity > 3 || max_unique < 1 || !cross_out) {
+        set_error("wj_join_cross: arity must be 2 or 3, max_unique >= 1");
+        return arity == 1 ? WJ_ERR_UNSUPPORTED : WJ_ERR_ARG;
+    }
+    if (n_batch == 0) return WJ_OK;
+    const size_t smem = (size_t)arity * max_unique * 8;
+    if (smem > 200 * 1024) {
+        set_error("wj_join_cross needs %zu B of shared memory", smem);
+        return WJ_ERR_UNSUPPORTED;
+    }
+    cudaError_t e;
+    if (arity == 2) {
+        cudaFuncSetAttribute(join_cross_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        e = launch_pdl(join_cross_kernel<2>, dim3((unsigned)n_batch), dim3(128), smem, (cudaStream_t)stream, queries,
+                       n_batch, offsets, uniq_x, uniq_id, (int)max_unique, cross_out);
+    } else {
+        cudaFuncSetAttribute(join_cross_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        e = launch_pdl(join_cross_kernel<3>, dim3((unsigned)n_batch), dim3(128), smem, (cudaStream_t)stream, queries,
+                       n_batch, offsets, uniq_x, uniq_id, (int)max_unique, cross_out);
+    }
+    if (e != cudaSuccess) {
+        set_error("wj_join_cross launch: %s", cudaGetErrorString(e));
+        return WJ_ERR_CUDA;
+    }
+    return check_launch("wj_join_cross");
+}

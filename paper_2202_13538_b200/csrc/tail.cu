@@ -21,9 +21,7 @@
 
 namespace wj {
 
-constexpr int kTailWarps = 8;
 constexpr int kH = 64;
-constexpr int kPitch = 65;
 
 struct ParamOffsets {
     int w1, b1, w2, b2, u1, c1, u2, c2, total;

@@ -144,11 +144,29 @@ def forward(p: ModelParams, dense: torch.Tensor, training: bool = False,
     return logits, cache
 
 
+def join_cross(store, q: torch.Tensor, out: Optional[torch.Tensor] = None) -> Optional[torch.Tensor]:
+    """Cross RPE ids of every distinct landing of every query anchor
+    (wj_join_cross): [B, A, A-1, max_unique] int32, or None for A = 1."""
+    from . import _lib
+
+    B, A = q.shape
+    if A < 2:
+        return None
+    mu = max(store.max_unique, 1)
+    if out is None:
+        out = torch.empty((B, A, A - 1, mu), dtype=torch.int32, device=store.device)
+    _lib.call("wj_join_cross", _lib.ptr(q), B, A, _lib.ptr(store.offsets_d), _lib.ptr(store.uniq_x_d),
+              _lib.ptr(store.uniq_id_d), mu, _lib.ptr(out), _lib.stream_handle(store.device))
+    return out
+
+
 def join_encode(store, q: torch.Tensor, w1: torch.Tensor, b1: torch.Tensor, keep: float, seed: int,
                 step: Optional[torch.Tensor], pooled: torch.Tensor, S: Optional[torch.Tensor] = None,
-                msum: Optional[torch.Tensor] = None, simt: bool = False) -> None:
+                msum: Optional[torch.Tensor] = None, simt: bool = False,
+                cross: Optional[torch.Tensor] = None) -> None:
     """One wj_join_encode launch (wj_join_encode_simt with ``simt``) on the
-    current stream; see include/walkjoin_b200.h for the outputs."""
+    current stream; see include/walkjoin_b200.h for the outputs.  ``cross``
+    (from join_cross) lets the tensor-core kernel skip its list searches."""
     from . import _lib
 
     B, A = q.shape
@@ -160,7 +178,7 @@ def join_encode(store, q: torch.Tensor, w1: torch.Tensor, b1: torch.Tensor, keep
     if simt:
         _lib.call("wj_join_encode_simt", *args, *tail)
     else:
-        _lib.call("wj_join_encode", *args, *store.vindex_ptrs(), *tail)
+        _lib.call("wj_join_encode", *args, _lib.ptr(cross), *store.vindex_ptrs(), *tail)
 
 
 def forward_fused(p: ModelParams, store, q: torch.Tensor, training: bool = False, seed: int = 0,
@@ -196,7 +214,7 @@ def forward_fused(p: ModelParams, store, q: torch.Tensor, training: bool = False
             S = torch.empty((B, AW, H), dtype=torch.float32, device=dev)
             msum = torch.empty((B, H), dtype=torch.float32, device=dev)
     t = p.tensors
-    join_encode(store, q, t["w1"], t["b1"], keep, seed, step, pooled, S, msum)
+    join_encode(store, q, t["w1"], t["b1"], keep, seed, step, pooled, S, msum, cross=o.get("cross"))
     if not tail:
         return None, None
     pooled_mean = pooled / (keep * rows)

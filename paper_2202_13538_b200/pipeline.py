@@ -250,18 +250,15 @@ class TrainStep:
 
     def _buffers(self, B, A):
         if self.mode == "fused":
-            if self.fast_tail:
-                # gradient CTAs of 16 queries each (fixed-order partial rows)
-                rows = max(1, min((B + 15) // 16, self.tail_rows))
-                H, AW = self.params.hidden, A * self.store.width
-                return {"pooled": torch.empty((B, H), device=self.dev),
-                        "S": torch.empty((B, AW, H), device=self.dev),
-                        "msum": torch.empty((B, H), device=self.dev),
-                            "partial": torch.empty((rows, int(self.offs[-1]) + 1), device=self.dev)}
             H, AW = self.params.hidden, A * self.store.width
-            return {"pooled": torch.empty((B, H), device=self.dev),
+            bufs = {"pooled": torch.empty((B, H), device=self.dev),
                     "S": torch.empty((B, AW, H), device=self.dev),
                     "msum": torch.empty((B, H), device=self.dev)}
+            if self.fast_tail:
+                # tail CTAs of 16 queries each (fixed-order partial rows)
+                rows = max(1, min((B + 15) // 16, self.tail_rows))
+                bufs["partial"] = torch.empty((rows, int(self.offs[-1]) + 1), device=self.dev)
+            return bufs
         d = 0 if self.features is None else int(self.features.shape[1])
         return {"dense": torch.empty((B, A * self.store.landings, A * self.store.width + d),
                                      dtype=self.dense_dtype, device=self.dev)}

@@ -37,9 +37,13 @@ def main():
     ms = torch.empty((B, 64), device=dev)
     t = p.tensors
 
+    cross = torch.empty((B, 2, 1, store.max_unique), dtype=torch.int32, device=dev)
+    use_cross = os.environ.get("WJ_CROSS") is not None  # precomputed cross ids (else in-kernel merge)
+
     def run():
         for q in qd:
-            wj.encoder.join_encode(store, q, t["w1"], t["b1"], 0.9, 5, step_t, pooled, S, ms)
+            c = wj.encoder.join_cross(store, q, cross[: q.shape[0]]) if use_cross else None
+            wj.encoder.join_encode(store, q, t["w1"], t["b1"], 0.9, 5, step_t, pooled, S, ms, cross=c)
 
     run()
     torch.cuda.synchronize()
@@ -52,8 +56,17 @@ def main():
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1) / len(qd))
     ms_k = min(times)
-    print(json.dumps({"config": a.config, "warps": os.environ.get("WJ_ENC_WARPS", "default"),
-                      "kernel_ms": round(ms_k, 4), "mu": store.max_unique,
+    # the cross-id kernel alone
+    tc = []
+    for _ in range(a.repeat):
+        e0.record()
+        for q in qd:
+            wj.encoder.join_cross(store, q, cross[: q.shape[0]])
+        e1.record()
+        torch.cuda.synchronize()
+        tc.append(e0.elapsed_time(e1) / len(qd))
+    print(json.dumps({"config": a.config, "cfg": os.environ.get("WJ_ENC_CFG", "default"), "cross": use_cross,
+                      "kernel_ms": round(ms_k, 4), "cross_ms": round(min(tc), 4), "mu": store.max_unique,
                       "q_per_batch": sum(q.shape[0] for q in qd) / len(qd)}))
 
 

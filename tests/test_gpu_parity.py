@@ -550,3 +550,29 @@ def test_fast_tail_matches_torch_tail(wj):
     for k in out[0][1]:
         torch.testing.assert_close(out[0][1][k], out[1][1][k], rtol=1e-4, atol=2e-6)
         torch.testing.assert_close(out[0][2][k], out[1][2][k], rtol=2e-3, atol=1e-7)
+
+
+@pytest.mark.parametrize("arity", [2, 3])
+def test_join_cross_matches_sorted_lookup(wj, arity):
+    """wj_join_cross (merge path) == the RPE id of every landing of every
+    anchor relative to every other anchor, by host binary search."""
+    g = _er(1_500, 12_000, 7)
+    s = wj.preprocess(g, 40, 3, 17)
+    rng = np.random.default_rng(5)
+    q = np.stack([rng.choice(1_500, arity, replace=False) for _ in range(64)]).astype(np.int64)
+    q[0, 1] = q[0, 0]  # repeated anchor: every landing matches itself
+    cross = wj.encoder.join_cross(s, torch.from_numpy(q).cuda()).cpu().numpy()
+    off = s.offsets_d.cpu().numpy()
+    ux = s.uniq_x_d.cpu().numpy()
+    uid = s.uniq_id_d.cpu().numpy()
+    for b in range(q.shape[0]):
+        for a in range(arity):
+            xa = ux[off[q[b, a]]:off[q[b, a] + 1]]
+            others = [j for j in range(arity) if j != a]
+            for jj, j in enumerate(others):
+                xj = ux[off[q[b, j]]:off[q[b, j] + 1]]
+                ij = uid[off[q[b, j]]:off[q[b, j] + 1]]
+                pos = np.searchsorted(xj, xa)
+                pc = np.minimum(pos, len(xj) - 1)
+                want = np.where((pos < len(xj)) & (xj[pc] == xa), ij[pc], 0)
+                np.testing.assert_array_equal(cross[b, a, jj, :len(xa)], want)
