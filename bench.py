@@ -315,8 +315,9 @@ def run_ours(args, cfg):
     h2d = int(np.mean([qh[k].numel() * 8 + yh[k].numel() * 4 for k in range(W, W + K)]))
 
     if args.mode == "fused" and step.fast_tail:
-        launches_per_step = 4
-        launches_note = "per timed step: wj_join_encode, tail_vec, tail_grad, wj_adam"
+        launches_per_step = 3
+        launches_note = ("per timed step (one CUDA graph, PDL-chained): wj_join_encode (join + layer 1), "
+                         "wj_encoder_tail (tensor-core tail + partial grads), wj_adam")
     else:
         launches_per_step = 1
         launches_note = "per timed step: wj_join (the encoder runs as PyTorch/cuBLAS kernels)"
@@ -337,7 +338,11 @@ def run_ours(args, cfg):
     # (uniq_x, uniq_id) lists in, pooled/msum/S out (the dense tile and the
     # [rows, 64] activations never exist)
     AW = A * (L + 1)
-    enc_bytes_q = A * 8 + A * ubar * 8 + (2 + AW) * 64 * 4
+    vbar = (store.vslots_d.numel() - 2) / store.num_nodes if store.vslots_d is not None else 0.0
+    # per query: query ids + per-anchor offsets / vindex entries, the anchors'
+    # sorted (uniq_x, uniq_id) lists, their virtual-landing lists (uint16);
+    # written: pooled, msum and S (fp32)
+    enc_bytes_q = A * (8 + 16 + 16) + A * ubar * 8 + A * vbar * 2 + (2 + AW) * 64 * 4
     kname = "wj_join_encode" if args.mode == "fused" else "wj_join"
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"{args.config}_{kname}_traffic.json")
@@ -353,7 +358,9 @@ def run_ours(args, cfg):
                 "frac": round(enc_bytes_q * B_mean / t_enc / 1e9 / hbm, 4), "traffic": traffic,
                 "bytes_per_query": round(enc_bytes_q, 1), "kernel_ms": round(t_enc * 1e3, 4),
                 "kernel_share_of_step": round(t_enc / t_step, 3),
-                "note": "issue-bound (dropout RNG + sparse FMA), not HBM-bound: see DESIGN.md"}
+                "note": ("issue-bound on the integer ALU (dropout hash) and latency-bound in the per-query "
+                         "prepass, not HBM-bound: it reads ~12 KB per query; see DESIGN.md"),
+                "traffic_note": "ncu dram bytes of one launch (profiles/c3_wj_join_encode_traffic.json)"}
     else:
         roof = {"kernel": "wj_join (join + densify, fp32 dense)", "bound": "hbm",
                 "achieved": round(achieved, 1), "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
