@@ -222,7 +222,7 @@ def run_ours(args, cfg):
     state = wj.AdamState.for_params(params, lr=1e-3)
     step = wj.TrainStep(store, params, state, dense_dtype=torch.float32, mode=args.mode,
                         use_graph=True, process_group=(dist.group.WORLD if world > 1 else None),
-                        seed=1000 + rank)
+                        seed=1000 + rank, overlap_inputs=True)
     for k in range(W):                       # warm-up: captures every batch shape of the plan
         step(qd[k], yd[k])
     for k in range(W, W + K):
@@ -294,7 +294,7 @@ def run_ours(args, cfg):
     state = wj.AdamState.for_params(params, lr=1e-3)
     step = wj.TrainStep(store, params, state, dense_dtype=torch.float32, mode=args.mode,
                         use_graph=True, process_group=(dist.group.WORLD if world > 1 else None),
-                        seed=1000 + rank)
+                        seed=1000 + rank, overlap_inputs=True)
     qh =[torch.from_numpy(q).pin_memory() for q, _ in plan]
     yh = [torch.from_numpy(y).pin_memory() for _, y in plan]
     loss_h = torch.empty(W + K, dtype=torch.float32).pin_memory()

@@ -203,18 +203,24 @@ def make_batch(index, positives: np.ndarray, pos_filter, cfg: TrainConfig, rng, 
 
 
 class TrainStep:
-    """One training step on the device, captured as a CUDA graph per batch
-    shape (``use_graph``).
+    """One training step on the device, captured as CUDA graphs per batch
+    shape (``use_graph``; two graphs with their own input buffers, so the
+    next batch's copy overlaps the current step on a side stream).
 
     mode="fused" (default): wj_join_encode (join + densify + layer 1 + ReLU +
-    dropout + row mean + backward statistics, one kernel) -> [B, 64] tail in
-    PyTorch -> BCE -> backward -> Adam.  mode="pooled" / "reference": the
-    wj_join dense kernel feeds the PyTorch encoder (``E.forward``)."""
+    dropout + row mean + backward statistics, one kernel) -> wj_encoder_tail
+    (tensor-core tail + partial gradients) -> wj_adam, PDL-chained (the
+    PyTorch tail is used for hidden != 64).  mode="pooled" / "reference": the
+    wj_join dense kernel feeds the PyTorch encoder (``E.forward``).
+
+    overlap_inputs: device-resident q / y are complete when passed (their
+    producers finished), so their copy need not wait for the current stream;
+    host (pinned) inputs always overlap."""
 
     def __init__(self, store: SubgraphStore, params: E.ModelParams, state: E.AdamState,
                  dense_dtype=torch.float32, mode: str = "fused", use_graph: bool = True,
                  process_group=None, seed: int = 0, fast_tail: Optional[bool] = None,
-                 features: Optional[torch.Tensor] = None):
+                 features: Optional[torch.Tensor] = None, overlap_inputs: bool = False):
         if features is not None and mode == "fused":
             raise ValueError("node features need mode='pooled' or 'reference' (the fused kernel is RPE-only)")
         self.store, self.params, self.state = store, params, state
@@ -227,6 +233,9 @@ class TrainStep:
         self._host_bc = torch.ones(2, dtype=params.w1.dtype).pin_memory()
         self.step_t = torch.zeros(1, dtype=torch.int64, device=self.dev)
         self._graphs: dict = {}
+        self._slot: dict = {}
+        self._copy_stream = torch.cuda.Stream(self.dev) if use_graph else None
+        self.overlap_inputs = bool(overlap_inputs)
         # fused + hidden 64: tail and Adam as two CUDA kernels on flat buffers
         self.fast_tail = (mode == "fused" and params.hidden == 64 and params.feature_dim == 0
                           and params.w1.dtype == torch.float32
@@ -332,13 +341,32 @@ class TrainStep:
             self.params.version += 1
             return out
         key = (B, A)
-        g = self._graphs.get(key)
-        if g is None:
-            g = self._capture(B, A)
-            self._graphs[key] = g
-        g["q"].copy_(q, non_blocking=True)
-        g["y"].copy_(y, non_blocking=True)
+        slots = self._graphs.get(key)
+        if slots is None:  # two captured graphs with their own input buffers
+            slots = [self._capture(B, A) for _ in range(2)]
+            self._graphs[key] = slots
+        i = self._slot.get(key, 0)
+        self._slot[key] = i ^ 1
+        g = slots[i]
+        cur = torch.cuda.current_stream(self.dev)
+        cs = self._copy_stream
+        # the batch is copied into this slot on a side stream, overlapping the
+        # previous step's kernels; the copy waits only for the replay that last
+        # read this slot (and, for device inputs not declared ready, for the
+        # current stream)
+        if q.device.type == "cuda" and not self.overlap_inputs:
+            cs.wait_stream(cur)
+        cs.wait_event(g["done"])
+        with torch.cuda.stream(cs):
+            g["q"].copy_(q, non_blocking=True)
+            g["y"].copy_(y, non_blocking=True)
+            g["ready"].record(cs)
+        for t in (q, y):
+            if t.device.type == "cuda":
+                t.record_stream(cs)
+        cur.wait_event(g["ready"])
         g["graph"].replay()
+        g["done"].record(cur)
         self.params.version += 1
         return g["loss"]
 
@@ -368,7 +396,8 @@ class TrainStep:
             self.state.m[k].copy_(snap_m[k])
             self.state.v[k].copy_(snap_v[k])
         self.step_t.copy_(snap_step)
-        return {"graph": graph, "q": q, "y": y, "bufs": bufs, "loss": loss}
+        return {"graph": graph, "q": q, "y": y, "bufs": bufs, "loss": loss, "ready": torch.cuda.Event(),
+                "done": torch.cuda.Event()}
 
 
 @dataclass

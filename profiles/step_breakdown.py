@@ -38,10 +38,10 @@ def main():
     yd = [torch.from_numpy(y).to(dev) for _, y in plan]
     p = wj.init_params(2, cfg["L"], dropout=0.1, seed=11, device=dev)
     st = wj.AdamState.for_params(p)
-    step = wj.TrainStep(store, p, st, use_graph=True, seed=3)
+    step = wj.TrainStep(store, p, st, use_graph=True, seed=3, overlap_inputs=True)
     for k in range(4):
         step(qd[k], yd[k])
-    g = step._graphs[(qd[0].shape[0], 2)]
+    g = step._graphs[(qd[0].shape[0], 2)][0]
     out = {
         "step_us": timed(lambda: step(qd[0], yd[0]), 50),
         "replay_us": timed(lambda: g["graph"].replay(), 50),
