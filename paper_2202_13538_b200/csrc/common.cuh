@@ -70,6 +70,9 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
                  "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+// wait until at most one committed group (the most recent) is still in flight
+__device__ __forceinline__ void cp_async_wait_group1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
 // Programmatic dependent launch (PDL): a kernel launched with
 // launch_pdl() may start while its stream predecessor is still running; it

@@ -144,11 +144,18 @@ __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], 
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-// acc[nt] += A[16 x 8KS] B[8KS x 8NT] for one warp; la(m, k) = A[m][k],
-// lb(k, nt) = B[k][8 nt + gq]
+// acc[nt] += A[16 x 8KS] B[8KS x 8NT] for one warp, via mo / no row / column
+// offsets; la(m, k) = A[m][k], lb(k, n) = B[k][n].  Even and odd k-steps
+// accumulate into separate fragments (two independent MMA chains), added at
+// the end.
 template <int NT, int KS, class LA, class LB>
 __device__ __forceinline__ void warp_mma3(float (&acc)[NT][4], int lane, LA la, LB lb) {
     const int gq = lane >> 2, tq = lane & 3;
+    float acc2[NT][4];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc2[nt][r] = 0.f;
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
         uint32_t ah[4], al[4];
@@ -159,26 +166,34 @@ __device__ __forceinline__ void warp_mma3(float (&acc)[NT][4], int lane, LA la, 
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
             uint32_t bh0, bl0, bh1, bl1;
-            tf32_split(lb(8 * ks + tq, nt), bh0, bl0);
-            tf32_split(lb(8 * ks + tq + 4, nt), bh1, bl1);
-            mma_tf32(acc[nt], al, bh0, bh1);
-            mma_tf32(acc[nt], ah, bl0, bl1);
-            mma_tf32(acc[nt], ah, bh0, bh1);
+            tf32_split(lb(8 * ks + tq, 8 * nt + gq), bh0, bl0);
+            tf32_split(lb(8 * ks + tq + 4, 8 * nt + gq), bh1, bl1);
+            float(&d)[4] = (ks & 1) ? acc2[nt] : acc[nt];
+            mma_tf32(d, al, bh0, bh1);
+            mma_tf32(d, ah, bl0, bl1);
+            mma_tf32(d, ah, bh0, bh1);
         }
     }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[nt][r] += acc2[nt][r];
 }
 
+constexpr int kTW = 8;  // warps per tail CTA
+
 template <int AW>
-__global__ void __launch_bounds__(128) tail_tc_kernel(TailArgs g) {
+__global__ void __launch_bounds__(kTW * 32) tail_tc_kernel(TailArgs g) {
+    constexpr int NT = kTW * 32;
     extern __shared__ __align__(16) float tsm[];
     float *W2s = tsm, *U1s = W2s + 64 * kTP;               // [64][kTP] row-major W2, U1
     float *PM = U1s + 64 * kTP, *HQ = PM + kTQ * kTP, *Z2 = HQ + kTQ * kTP;
     float *DZ2 = Z2 + kTQ * kTP, *DHQ = DZ2 + kTQ * kTP, *G = DHQ + kTQ * kTP;  // [kTQ][kTP] each
-    float *vsm = G + kTQ * kTP;                             // [4 warps][64] du2 partials | dl | loss
-    float *SS = vsm + 272;                                  // [kTQ][(AW+1)*64] S | msum of the chunk
+    float *vsm = G + kTQ * kTP;                             // [kTW][64] du2 partials | dc2 | loss
+    float *SS = vsm + kTW * 64 + 2 * kTW;                   // [kTQ][(AW+1)*64] S | msum of the chunk
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
     const float *P = g.params;
-    for (int i = tid; i < 64 * 16; i += 128) {
+    for (int i = tid; i < 64 * 16; i += NT) {
         const int r = i >> 4, c = (i & 15) * 4;
         cp_async16(W2s + r * kTP + c, P + g.off.w2 + r * 64 + c);
         cp_async16(U1s + r * kTP + c, P + g.off.u1 + r * 64 + c);
@@ -189,51 +204,57 @@ __global__ void __launch_bounds__(128) tail_tc_kernel(TailArgs g) {
     const bool train = g.labels != nullptr;
     const int64_t q_lo = (int64_t)blockIdx.x * g.per_cta;
     const int64_t q_hi = min(g.B, q_lo + g.per_cta);
-    constexpr int NW1 = ((AW + 1) * 64 + 127) / 128;
-    float aw2[8][4], au1[8][4], aw1[NW1], vacc = 0.f, du2a = 0.f, du2b = 0.f, dc2 = 0.f, lsum = 0.f;
+    constexpr int NW1 = ((AW + 1) * 64 + NT - 1) / NT;
+    // dW2 / dU1 tiles of this warp: m-tile (warp & 3), n-tiles 4 (warp >> 2) .. +3
+    const int fm = warp & 3, fn = (warp >> 2) * 4;
+    float aw2[4][4], au1[4][4], aw1[NW1], vacc = 0.f, du2a = 0.f, du2b = 0.f, dc2 = 0.f, lsum = 0.f;
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int r = 0; r < 4; ++r) aw2[i][r] = au1[i][r] = 0.f;
 #pragma unroll
     for (int i = 0; i < NW1; ++i) aw1[i] = 0.f;
-    cp_async_wait_all();
-    __syncthreads();
     for (int64_t q0 = q_lo; q0 < q_hi; q0 += kTQ) {
         const int nq = (int)min((int64_t)kTQ, q_hi - q0);
-        if (train) {  // the chunk's S and msum, in flight while the products run
-            for (int i = tid; i < nq * AW * 16; i += 128) {
+        // the chunk's pooled rows (unscaled: the scale is applied to hq and dW2)
+        for (int i = tid; i < kTQ * 16; i += NT) {
+            const int q = i >> 4, c = (i & 15) * 4;
+            if (q < nq)
+                cp_async16(PM + q * kTP + c, g.pooled + (q0 + q) * 64 + c);
+            else
+                *reinterpret_cast<float4 *>(PM + q * kTP + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        cp_async_commit();  // group: pooled rows (+ W2 / U1 on the first chunk)
+        if (train) {  // S and msum, in flight while the products run
+            for (int i = tid; i < nq * AW * 16; i += NT) {
                 const int q = i / (AW * 16), c = i - q * AW * 16;
                 cp_async16(SS + q * (AW + 1) * 64 + c * 4, g.s + (q0 + q) * AW * 64 + c * 4);
             }
-            for (int i = tid; i < nq * 16; i += 128)
+            for (int i = tid; i < nq * 16; i += NT)
                 cp_async16(SS + (i >> 4) * (AW + 1) * 64 + AW * 64 + (i & 15) * 4, g.msum + (q0 + (i >> 4)) * 64 + (i & 15) * 4);
+            cp_async_commit();
         }
-        for (int i = tid; i < kTQ * 64; i += 128) {
-            const int q = i >> 6, k = i & 63;
-            PM[q * kTP + k] = q < nq ? g.pooled[(q0 + q) * 64 + k] * g.scale : 0.f;
-        }
+        // wait for W2 / U1 (first chunk) and the pooled rows; S may still be in flight
+        if (train) cp_async_wait_group1(); else cp_async_wait_all();
         __syncthreads();
-        // hq = pm W2 + b2 ; z2 = hq U1 + c1   (warp w: output columns 16w .. 16w+15)
+        // hq = scale * pooled W2 + b2 ; z2 = hq U1 + c1   (warp w: output columns 8w .. 8w+7)
 #pragma unroll
         for (int pass = 0; pass < 2; ++pass) {
             const float *X = pass ? HQ : PM, *M = pass ? U1s : W2s, *bias = P + (pass ? g.off.c1 : g.off.b2);
+            const float mul = pass ? 1.f : g.scale;
             float *Y = pass ? Z2 : HQ;
-            float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-            warp_mma3<2, 8>(acc, lane, [&](int m, int k) { return X[m * kTP + k]; },
-                            [&](int k, int nt) { return M[k * kTP + 16 * warp + 8 * nt + gq]; });
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt) {
-                const int c = 16 * warp + 8 * nt + 2 * tq;
-                Y[gq * kTP + c] = acc[nt][0] + bias[c];
-                Y[gq * kTP + c + 1] = acc[nt][1] + bias[c + 1];
-                Y[(gq + 8) * kTP + c] = acc[nt][2] + bias[c];
-                Y[(gq + 8) * kTP + c + 1] = acc[nt][3] + bias[c + 1];
-            }
+            float acc[1][4] = {{0.f, 0.f, 0.f, 0.f}};
+            warp_mma3<1, 8>(acc, lane, [&](int m, int k) { return X[m * kTP + k]; },
+                            [&](int k, int n) { return M[k * kTP + 8 * warp + n]; });
+            const int c = 8 * warp + 2 * tq;
+            Y[gq * kTP + c] = fmaf(acc[0][0], mul, bias[c]);
+            Y[gq * kTP + c + 1] = fmaf(acc[0][1], mul, bias[c + 1]);
+            Y[(gq + 8) * kTP + c] = fmaf(acc[0][2], mul, bias[c]);
+            Y[(gq + 8) * kTP + c + 1] = fmaf(acc[0][3], mul, bias[c + 1]);
             __syncthreads();
         }
-        // logits, BCE and dz2 (warp w: queries w, w+4, w+8, w+12)
-        for (int q = warp; q < kTQ; q += 4) {
+        // logits, BCE and dz2 (warp w: queries w, w + 8)
+        for (int q = warp; q < kTQ; q += kTW) {
             const float za = Z2[q * kTP + lane], zb = Z2[q * kTP + lane + 32];
             float part = fmaxf(za, 0.f) * u2a + fmaxf(zb, 0.f) * u2b;
 #pragma unroll
@@ -265,37 +286,34 @@ __global__ void __launch_bounds__(128) tail_tc_kernel(TailArgs g) {
             const float *X = pass ? DHQ : DZ2, *M = pass ? W2s : U1s;
             float *Y = pass ? G : DHQ;
             const float mul = pass ? g.scale : 1.f;
-            float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-            warp_mma3<2, 8>(acc, lane, [&](int m, int k) { return X[m * kTP + k]; },
-                            [&](int k, int nt) { return M[(16 * warp + 8 * nt + gq) * kTP + k]; });
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt) {
-                const int c = 16 * warp + 8 * nt + 2 * tq;
-                Y[gq * kTP + c] = acc[nt][0] * mul;
-                Y[gq * kTP + c + 1] = acc[nt][1] * mul;
-                Y[(gq + 8) * kTP + c] = acc[nt][2] * mul;
-                Y[(gq + 8) * kTP + c + 1] = acc[nt][3] * mul;
-            }
+            float acc[1][4] = {{0.f, 0.f, 0.f, 0.f}};
+            warp_mma3<1, 8>(acc, lane, [&](int m, int k) { return X[m * kTP + k]; },
+                            [&](int k, int n) { return M[(8 * warp + n) * kTP + k]; });
+            const int c = 8 * warp + 2 * tq;
+            Y[gq * kTP + c] = acc[0][0] * mul;
+            Y[gq * kTP + c + 1] = acc[0][1] * mul;
+            Y[(gq + 8) * kTP + c] = acc[0][2] * mul;
+            Y[(gq + 8) * kTP + c + 1] = acc[0][3] * mul;
             __syncthreads();
         }
-        // dW2 += pm^T dhq, dU1 += hq^T dz2  (warp w: rows 16w .. 16w+15, all 64 columns)
-        warp_mma3<8, 2>(aw2, lane, [&](int m, int k) { return PM[k * kTP + 16 * warp + m]; },
-                        [&](int k, int nt) { return DHQ[k * kTP + 8 * nt + gq]; });
-        warp_mma3<8, 2>(au1, lane, [&](int m, int k) { return HQ[k * kTP + 16 * warp + m]; },
-                        [&](int k, int nt) { return DZ2[k * kTP + 8 * nt + gq]; });
+        // dW2 += pooled^T dhq (scaled at the end), dU1 += hq^T dz2
+        warp_mma3<4, 2>(aw2, lane, [&](int m, int k) { return PM[k * kTP + 16 * fm + m]; },
+                        [&](int k, int n) { return DHQ[k * kTP + 8 * fn + n]; });
+        warp_mma3<4, 2>(au1, lane, [&](int m, int k) { return HQ[k * kTP + 16 * fm + m]; },
+                        [&](int k, int n) { return DZ2[k * kTP + 8 * fn + n]; });
         // dW1[c][h] += S_q[c][h] g_q[h], db1[h] += msum_q[h] g_q[h]; db2 = sum dhq, dc1 = sum dz2
         cp_async_wait_all();
         __syncthreads();
 #pragma unroll
         for (int i = 0; i < NW1; ++i) {
-            const int e = tid + 128 * i;
+            const int e = tid + NT * i;
             if (e < (AW + 1) * 64) {
                 float a = aw1[i];
                 for (int q = 0; q < nq; ++q) a = fmaf(SS[q * (AW + 1) * 64 + e], G[q * kTP + (e & 63)], a);
                 aw1[i] = a;
             }
         }
-        {
+        if (tid < 128) {
             const float *V = tid < 64 ? DHQ : DZ2;
             for (int q = 0; q < nq; ++q) vacc += V[q * kTP + (tid & 63)];
         }
@@ -306,40 +324,53 @@ __global__ void __launch_bounds__(128) tail_tc_kernel(TailArgs g) {
     // ---- partial row of this CTA: [grads | loss]
     float *row = g.partial + (int64_t)blockIdx.x * (g.off.total + 1);
 #pragma unroll
-    for (int nt = 0; nt < 8; ++nt) {
-        const int r0 = 16 * warp + gq, c = 8 * nt + 2 * tq;
-        row[g.off.w2 + r0 * 64 + c] = aw2[nt][0];
-        row[g.off.w2 + r0 * 64 + c + 1] = aw2[nt][1];
-        row[g.off.w2 + (r0 + 8) * 64 + c] = aw2[nt][2];
-        row[g.off.w2 + (r0 + 8) * 64 + c + 1] = aw2[nt][3];
-        row[g.off.u1 + r0 * 64 + c] = au1[nt][0];
-        row[g.off.u1 + r0 * 64 + c + 1] = au1[nt][1];
-        row[g.off.u1 + (r0 + 8) * 64 + c] = au1[nt][2];
-        row[g.off.u1 + (r0 + 8) * 64 + c + 1] = au1[nt][3];
+    for (int j = 0; j < 4; ++j) {
+        const int r0 = 16 * fm + gq, c = 8 * (fn + j) + 2 * tq;
+        row[g.off.w2 + r0 * 64 + c] = aw2[j][0] * g.scale;
+        row[g.off.w2 + r0 * 64 + c + 1] = aw2[j][1] * g.scale;
+        row[g.off.w2 + (r0 + 8) * 64 + c] = aw2[j][2] * g.scale;
+        row[g.off.w2 + (r0 + 8) * 64 + c + 1] = aw2[j][3] * g.scale;
+        row[g.off.u1 + r0 * 64 + c] = au1[j][0];
+        row[g.off.u1 + r0 * 64 + c + 1] = au1[j][1];
+        row[g.off.u1 + (r0 + 8) * 64 + c] = au1[j][2];
+        row[g.off.u1 + (r0 + 8) * 64 + c + 1] = au1[j][3];
     }
 #pragma unroll
     for (int i = 0; i < NW1; ++i) {
-        const int e = tid + 128 * i;
+        const int e = tid + NT * i;
         if (e < AW * 64)
             row[g.off.w1 + e] = aw1[i];
         else if (e < (AW + 1) * 64)
             row[g.off.b1 + e - AW * 64] = aw1[i];
     }
-    row[(tid < 64 ? g.off.b2 : g.off.c1) + (tid & 63)] = vacc;
+    if (tid < 128) row[(tid < 64 ? g.off.b2 : g.off.c1) + (tid & 63)] = vacc;
     vsm[warp * 64 + lane] = du2a;
     vsm[warp * 64 + lane + 32] = du2b;
     if (lane == 0) {
-        vsm[256 + warp] = dc2;
-        vsm[260 + warp] = lsum;
+        vsm[kTW * 64 + warp] = dc2;
+        vsm[kTW * 64 + kTW + warp] = lsum;
     }
     __syncthreads();
-    if (tid < 64) row[g.off.u2 + tid] = (vsm[tid] + vsm[64 + tid]) + (vsm[128 + tid] + vsm[192 + tid]);
-    if (tid == 64) row[g.off.c2] = (vsm[256] + vsm[257]) + (vsm[258] + vsm[259]);
-    if (tid == 65) row[g.off.total] = ((vsm[260] + vsm[261]) + (vsm[262] + vsm[263])) * g.inv_b;
+    if (tid < 64) {
+        float v = 0.f;
+#pragma unroll
+        for (int w = 0; w < kTW; ++w) v += vsm[w * 64 + tid];
+        row[g.off.u2 + tid] = v;
+    } else if (tid == 64 || tid == 65) {
+        float v = 0.f;
+#pragma unroll
+        for (int w = 0; w < kTW; ++w) v += vsm[kTW * 64 + (tid - 64) * kTW + w];
+        if (tid == 64)
+            row[g.off.c2] = v;
+        else
+            row[g.off.total] = v * g.inv_b;
+    }
 }
 
 template <int AW>
-constexpr size_t tail_smem() { return (size_t)(2 * 64 * kTP + 6 * kTQ * kTP + 272 + kTQ * (AW + 1) * 64) * 4; }
+constexpr size_t tail_smem() {
+    return (size_t)(2 * 64 * kTP + 6 * kTQ * kTP + kTW * 64 + 2 * kTW + kTQ * (AW + 1) * 64) * 4;
+}
 
 using TailKernel = void (*)(TailArgs);
 
@@ -403,7 +434,7 @@ extern "C" int wj_encoder_tail(const float *pooled, const float *s, const float 
         set_error("tail smem attribute: %s", cudaGetErrorString(e));
         return WJ_ERR_CUDA;
     }
-    e = launch_pdl(k, dim3((unsigned)rows), dim3(128), smem, (cudaStream_t)stream, g);
+    e = launch_pdl(k, dim3((unsigned)rows), dim3(kTW * 32), smem, (cudaStream_t)stream, g);
     if (e != cudaSuccess) {
         set_error("wj_encoder_tail launch: %s", cudaGetErrorString(e));
         return WJ_ERR_CUDA;

@@ -324,11 +324,12 @@ class TrainStep:
 
     def _prepare_bc(self):
         self.state.step += 1
+        if self.fast_tail:  # the kernel path derives the corrections from the device step counter
+            return
         t = self.state.step
         self._host_bc[0] = 1.0 / (1.0 - self.state.beta1 ** t)
         self._host_bc[1] = 1.0 / (1.0 - self.state.beta2 ** t)
-        if not self.fast_tail:  # the kernel path derives the corrections from the device step counter
-            self.inv_bc.copy_(self._host_bc, non_blocking=True)
+        self.inv_bc.copy_(self._host_bc, non_blocking=True)
 
     def __call__(self, q: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
         """q: [B, A] int64 ids, y: [B] labels (device, or pinned host for the
