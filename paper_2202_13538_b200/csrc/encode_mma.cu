@@ -157,6 +157,7 @@ __device__ __forceinline__ void tile(const uint16_t *lst, uint32_t xr_s, uint32_
     uint32_t bx[4], bt[4];
     ldsm_x4(bx, row_addr(xr_s, ib, (lane >> 3) & 1));
     ldsm_x4_t(bt, row_addr(xr_s, it, lane >> 4));
+    const uint32_t cqk = cq * 0x7feb352dU;
     uint32_t ga[4][4];  // GEMM2 A fragments: G^T (unit x landing), fp16
     const int arow = (lane & 7) + 8 * ((lane >> 3) & 1), acol = 8 * (lane >> 4);
 #pragma unroll
@@ -172,9 +173,9 @@ __device__ __forceinline__ void tile(const uint16_t *lst, uint32_t xr_s, uint32_
             // z[r]: unit 16mt + gq + 8(r>>1), landing 8t + 2tq + (r&1)
 #pragma unroll
             for (int hb = 0; hb < 2; ++hb) {
-                // counter (t, mt, hb) bits are disjoint from cq's: one XOR
-                uint32_t x = cq ^ ((uint32_t)t << 8 | (uint32_t)mt << 4 | (uint32_t)hb << 3);
-                x *= 0x7feb352dU;
+                // hash of cq + counter (t, mt, hb): the first multiply and the
+                // counter fold into one IMAD with a compile-time addend
+                uint32_t x = cqk + ((uint32_t)t << 8 | (uint32_t)mt << 4 | (uint32_t)hb << 3) * 0x7feb352dU;
                 x ^= x >> 15;
                 x *= 0x846ca68bU;
                 const uint32_t up = ~(x ^ (x >> 16)) & 0x3FFF3FFFu;  // 0x3FFF - u, two lanes

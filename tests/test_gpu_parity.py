@@ -408,9 +408,14 @@ def _fused_model_mma(store, q, w1, b1, keep, seed, step):
         z = (b1[None, :].astype(np.float64) + X @ w1.astype(np.float64)).astype(np.float32)
         z[np.all(X == 0, axis=1)] = 0.0  # padding rows: contribute nothing
         v = np.arange(V, dtype=np.uint64)[:, None]
-        c = ((v >> np.uint64(1)) << np.uint64(6)) | (mt << np.uint64(4)) | (hb << np.uint64(3)) | gq
-        x = (np.uint64(qq) ^ c) & np.uint64(_M32)
-        x = (x * np.uint64(0x7FEB352D)) & np.uint64(_M32)
+        # per-tile part cq (landing tile v0, pair tq, unit row gq), plus the
+        # per-pair counter k (block t, unit tile mt, unit half hb)
+        tq = (v >> np.uint64(1)) & np.uint64(3)
+        v0 = v & ~np.uint64(15)
+        tt = (v >> np.uint64(3)) & np.uint64(1)
+        cq = (np.uint64(qq) ^ (v0 << np.uint64(5)) ^ (tq << np.uint64(6)) ^ gq) & np.uint64(_M32)
+        k = (tt << np.uint64(8)) | (mt << np.uint64(4)) | (hb << np.uint64(3))
+        x = ((cq + k) * np.uint64(0x7FEB352D)) & np.uint64(_M32)
         x ^= x >> np.uint64(15)
         x = (x * np.uint64(0x846CA68B)) & np.uint64(_M32)
         y = ~(x ^ (x >> np.uint64(16))) & np.uint64(0x3FFF3FFF)
