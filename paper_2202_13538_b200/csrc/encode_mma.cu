@@ -313,6 +313,25 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
     const uint32_t xr_s = smem_u32(xr), wt_s = smem_u32(wt);
     const uint32_t zrow = (uint32_t)(A * mu);  // all-zero row: padding (contributes nothing)
 
+    // metadata of the CTA's first kMetaQ queries: independent of the previous
+    // kernel in the stream, so it is fetched before the PDL wait
+    auto load_meta = [&](int64_t b0) {
+        for (int t = threadIdx.x; t < kMetaQ * A; t += NT) {
+            const int i = t / A, a = t - i * A;
+            const int64_t bb = b0 + (int64_t)i * gridDim.x;
+            QMeta m = {0, 0, 0, 0, 0};
+            if (bb < g.n_batch) {
+                const int64_t q = g.queries[bb * A + a];
+                m.lo = g.offsets[q];
+                m.u = (int)(g.offsets[q + 1] - m.lo);
+                m.vo = g.voff[q];
+                m.v2 = g.vcnt[2 * q];
+                m.v1 = g.vcnt[2 * q + 1];
+            }
+            meta[t] = m;
+        }
+    };
+    load_meta(blockIdx.x);
     pdl_wait();  // params / step counter come from the previous kernel in the stream
     const uint64_t skey = mix64(g.seed + kGolden * ((uint64_t)(g.step ? *g.step : 0) + 1ULL));
 
@@ -352,24 +371,9 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
     int jq = 0;  // local query index
     for (int64_t b = blockIdx.x; b < g.n_batch; b += gridDim.x, ++jq) {
         if (b + gridDim.x >= g.n_batch) pdl_trigger();  // last query of this CTA: dependents may launch
-        if (jq % kMetaQ == 0) {
-            // metadata of this CTA's next kMetaQ queries, loaded in one go
-            // (q -> offsets / vindex is a dependent pair of global reads)
+        if (jq > 0 && jq % kMetaQ == 0) {  // metadata of the CTA's next kMetaQ queries
             __syncthreads();
-            for (int t = threadIdx.x; t < kMetaQ * A; t += NT) {
-                const int i = t / A, a = t - i * A;
-                const int64_t bb = b + (int64_t)i * gridDim.x;
-                QMeta m = {0, 0, 0, 0, 0};
-                if (bb < g.n_batch) {
-                    const int64_t q = g.queries[bb * A + a];
-                    m.lo = g.offsets[q];
-                    m.u = (int)(g.offsets[q + 1] - m.lo);
-                    m.vo = g.voff[q];
-                    m.v2 = g.vcnt[2 * q];
-                    m.v1 = g.vcnt[2 * q + 1];
-                }
-                meta[t] = m;
-            }
+            load_meta(b);
             __syncthreads();
         }
         const QMeta *qm = meta + (jq % kMetaQ) * A;
