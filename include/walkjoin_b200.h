@@ -224,6 +224,19 @@ int wj_export_dicts(const int64_t *offsets, const int32_t *uniq_x, const int32_t
                     int32_t num_walks, int32_t num_steps, const int64_t *cap_offsets,
                     int32_t *dict_keys, int32_t *dict_vals, wj_stream_t stream);
 
+/* Reference store-file (SURL v1) node records as 4-byte words (store.py:
+ * 167-193, 204-264): record u at word rec_off[u] = capacity, walks[u]
+ * (walk_words = M*(L+1) int32), dict_keys, dict_vals of node u (capacity =
+ * dict_offsets[u+1] - dict_offsets[u]).  pack writes the records of n_nodes
+ * nodes; unpack reads walks (and, when dict_keys_out != NULL, the dicts)
+ * back.  The host writes / parses the header, table and id map. */
+int wj_surl_pack(const int32_t *walks, int64_t n_nodes, int32_t walk_words, const int64_t *dict_offsets,
+                 const int32_t *dict_keys, const int32_t *dict_vals, const int64_t *rec_off, int32_t *out,
+                 wj_stream_t stream);
+int wj_surl_unpack(const int32_t *records, int64_t n_nodes, int32_t walk_words, const int64_t *rec_off,
+                   const int64_t *dict_offsets, int32_t *walks_out, int32_t *dict_keys_out,
+                   int32_t *dict_vals_out, wj_stream_t stream);
+
 /* Point lookups out[i] = RPE id of x[i] relative to anchor u[i] (0 if
  * absent).  Replaces store.get_rpe_id / _kernels.dict_get_one
  * (store.py:160-164, _kernels.py:203-206). */

@@ -331,3 +331,31 @@ def dense_batch(store: OracleStore, query_array, threads=None, features=None):
         flat = walk_nodes.reshape(B, rows)
         dense = np.concatenate([dense, features[flat]], axis=2)
     return dense
+
+
+SURL_MAGIC, SURL_VERSION = b"SURL", 1
+
+
+def write_surl(store: OracleStore, id_map=None) -> bytes:
+    """Restatement of store._write_store (store.py:167-193): magic, the
+    little-endian header <IIIQQQQ (version, M, L, seed, n, |table|, |id_map|),
+    the table, then per node: capacity (u32), walks[u], dict_keys, dict_vals,
+    and finally the original ids (int64, dense order) when there is an id_map."""
+    import struct
+
+    n = store.num_nodes
+    id_len = n if id_map is not None else 0
+    parts = [SURL_MAGIC, struct.pack("<IIIQQQQ", SURL_VERSION, store.num_walks, store.walk_steps,
+                                     store.seed & _MASK64, n, store.table.shape[0], id_len),
+             np.ascontiguousarray(store.table, np.int32).tobytes()]
+    caps = np.diff(store.dict_offsets)
+    for u in range(n):
+        lo, hi = store.dict_offsets[u], store.dict_offsets[u + 1]
+        parts += [struct.pack("<I", int(caps[u])), store.walks[u].tobytes(),
+                  store.dict_keys[lo:hi].tobytes(), store.dict_vals[lo:hi].tobytes()]
+    if id_len:
+        origs = np.empty(n, np.int64)
+        for orig, dense in id_map.items():
+            origs[dense] = orig
+        parts.append(origs.tobytes())
+    return b"".join(parts)

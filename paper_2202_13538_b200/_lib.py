@@ -47,6 +47,8 @@ SIGNATURES = {
     "wj_gather_rpe": [P, I64, P, I64, I32, P, I32, P, P],
     "wj_export_dicts": [P, P, P, P, P, I64, I32, I32, P, P, P, P],
     "wj_lookup": [P, P, I64, P, P, P, P, P],
+    "wj_surl_pack": [P, I64, I32, P, P, P, P, P, P],
+    "wj_surl_unpack": [P, I64, I32, P, P, P, P, P, P],
 }
 
 _lib = None

@@ -179,6 +179,19 @@ def preprocess(g, num_walks: int, num_steps: int, seed: int, threads: int = 1,
     _lib.call("wj_sample_walks", _lib.ptr(dg.idxptr), dg.idxptr_bytes, _lib.ptr(dg.indices), n, 0, n,
               M, L, seed64, _lib.ptr(walks), _lib.ptr(flags), s)
     del flags
+    return store_from_walks(walks, n, M, L, seed64, id_map=getattr(g, "id_map", None), keep_keys=keep_keys,
+                            ph=ph)
+
+
+def store_from_walks(walks: torch.Tensor, n: int, M: int, L: int, seed64: int, id_map=None,
+                     keep_keys: bool = False, ph=None) -> SubgraphStore:
+    """Distinct landings + counts, global interning, virtual-landing index of
+    a device walk table [n, M, L+1] int32 (sampler.py:117-151 after
+    sampling); also the path of load_store."""
+    dev = walks.device
+    W = L + 1
+    s = _lib.stream_handle(dev)
+    ph = ph if ph is not None else _Phases(None)
     counts = torch.empty(n, dtype=torch.int32, device=dev)
     ph.mark("rpe_count")
     _lib.call("wj_rpe_count", _lib.ptr(walks), n, M, L, n, _lib.ptr(counts), s)
@@ -196,7 +209,7 @@ def preprocess(g, num_walks: int, num_steps: int, seed: int, threads: int = 1,
     ph.mark("intern")
     uid, table_keys = intern_device(ukey, ufirst, offsets, n, 0, M, W)
     store = SubgraphStore(n, M, L, seed64, walks, offsets, ux, uid, ufirst, slot, table_keys,
-                          max_unique, id_map=getattr(g, "id_map", None))
+                          max_unique, id_map=id_map)
     ph.mark("vindex")
     store.build_vindex()
     ph.mark("end")

@@ -182,7 +182,9 @@ class SubgraphStore:
             self._anchor_counts = (self.offsets_d[1:] - self.offsets_d[:-1]).to(torch.int64)
         return self._anchor_counts
 
-    def _export_dicts(self):
+    def export_dicts_device(self):
+        """The reference per-node dicts (store.py:124-131, _kernels.py:174-188)
+        on the device: (cap_offsets host int64 [n+1], cap_offsets, keys, vals)."""
         counts = self.anchor_counts().cpu().numpy()
         caps = dict_capacities(counts)
         cap_offsets = np.zeros(self.num_nodes + 1, np.int64)
@@ -195,6 +197,10 @@ class SubgraphStore:
                   _lib.ptr(self.uniq_id_d), _lib.ptr(self.uniq_first_d), _lib.ptr(self.slot_idx_d),
                   self.num_nodes, self.num_walks, self.walk_steps, _lib.ptr(cap_d), _lib.ptr(keys),
                   _lib.ptr(vals), _lib.stream_handle(dev))
+        return cap_offsets, cap_d, keys, vals
+
+    def _export_dicts(self):
+        cap_offsets, _, keys, vals = self.export_dicts_device()
         for k, a in (("dict_offsets", cap_offsets), ("dict_keys", keys.cpu().numpy()),
                      ("dict_vals", vals.cpu().numpy())):
             a.setflags(write=False)
@@ -285,3 +291,125 @@ def get_rpe_ids(store: SubgraphStore, u: torch.Tensor, x: torch.Tensor) -> torch
               _lib.ptr(store.uniq_x_d), _lib.ptr(store.uniq_id_d), _lib.ptr(out),
               _lib.stream_handle(store.device))
     return out
+
+
+# ------------------------------------------------------- store file (SURL) --
+_MAGIC = b"SURL"
+_VERSION = 1
+_HEADER = "<IIIQQQQ"
+
+
+def save_store(store: SubgraphStore, path, chunk_bytes: int = 1 << 28) -> None:
+    """Write the reference store file (store.py:167-201), byte-identical to
+    walkjoin.save_store of the same store: header, table, then per node
+    capacity, walks and the node's open-addressing dict, then the id map.
+    The node records are packed on the device (wj_surl_pack) in chunks of
+    about ``chunk_bytes``."""
+    import struct
+
+    n, M, L = store.num_nodes, store.num_walks, store.walk_steps
+    MW = M * (L + 1)
+    dev = store.device
+    cap_offsets, cap_d, keys, vals = store.export_dicts_device()
+    caps = np.diff(cap_offsets)
+    rec_words = 1 + MW + 2 * caps
+    id_len = n if store.id_map is not None else 0
+    table = store.table.vectors
+    s = _lib.stream_handle(dev)
+    with open(path, "wb") as fh:
+        fh.write(_MAGIC)
+        fh.write(struct.pack(_HEADER, _VERSION, M, L, store.seed & 0xFFFFFFFFFFFFFFFF, n, table.shape[0], id_len))
+        fh.write(np.ascontiguousarray(table, np.int32).tobytes())
+        u0 = 0
+        cum = np.zeros(n + 1, np.int64)
+        np.cumsum(rec_words, out=cum[1:])
+        limit = max(chunk_bytes // 4, int(rec_words.max()) if n else 1)
+        while u0 < n:
+            u1 = int(np.searchsorted(cum, cum[u0] + limit, side="right")) - 1
+            u1 = min(max(u1, u0 + 1), n)
+            rec_off = torch.from_numpy(cum[u0:u1] - cum[u0]).to(dev)
+            out = torch.empty(int(cum[u1] - cum[u0]), dtype=torch.int32, device=dev)
+            _lib.call("wj_surl_pack", store.walks_d.data_ptr() + 4 * u0 * MW, u1 - u0, MW,
+                      cap_d.data_ptr() + 8 * u0, _lib.ptr(keys), _lib.ptr(vals), _lib.ptr(rec_off),
+                      _lib.ptr(out), s)
+            fh.write(out.cpu().numpy().tobytes())
+            u0 = u1
+        if id_len:
+            origs = np.empty(n, np.int64)
+            for orig, dense in store.id_map.items():
+                origs[dense] = orig
+            fh.write(origs.tobytes())
+
+
+def load_store(path, device=None) -> SubgraphStore:
+    """Read a reference store file (store.py:204-264) into a device store.
+    Magic, version and lengths are checked like the reference
+    (StoreFormatError).  The walks are unpacked on the device and the index
+    is rebuilt from them; the rebuilt RPE table and per-node dicts must equal
+    the file's, else the file is inconsistent (StoreFormatError)."""
+    import struct
+
+    from .sampler import store_from_walks
+
+    dev = _lib.require_cuda(device)
+    with open(path, "rb") as fh:
+        data = fh.read()
+    if data[:4] != _MAGIC:
+        raise StoreFormatError(f"bad magic {data[:4]!r}, expected {_MAGIC!r}")
+    header_size = 4 + struct.calcsize(_HEADER)
+    if len(data) < header_size:
+        raise StoreFormatError("truncated store file (header)")
+    version, M, L, seed, n, table_len, id_len = struct.unpack_from(_HEADER, data, 4)
+    if version != _VERSION:
+        raise StoreFormatError(f"unsupported store version {version}, expected {_VERSION}")
+    W = L + 1
+    MW = M * W
+    off = header_size
+    tb = table_len * W * 4
+    if off + tb > len(data):
+        raise StoreFormatError("truncated store file")
+    table = np.frombuffer(data, np.int32, table_len * W, off).reshape(table_len, W)
+    off += tb
+    rec0 = off
+    caps = np.empty(n, np.int64)
+    unpack = struct.Struct("<I").unpack_from
+    size = len(data)
+    for u in range(n):  # records are variable-length: one sequential scan of the capacities
+        if off + 4 > size:
+            raise StoreFormatError("truncated store file")
+        cap = unpack(data, off)[0]
+        caps[u] = cap
+        off += 4 * (1 + MW + 2 * cap)
+    if off > size:
+        raise StoreFormatError("truncated store file")
+    rec_end = off
+    id_map = None
+    if id_len:
+        if off + 8 * id_len > size:
+            raise StoreFormatError("truncated store file")
+        origs = np.frombuffer(data, np.int64, id_len, off)
+        id_map = {int(o): d for d, o in enumerate(origs)}
+        off += 8 * id_len
+    if off != size:
+        raise StoreFormatError(f"store file has {size - off} trailing bytes")
+    rec_words = 1 + MW + 2 * caps
+    rec_off = np.zeros(n, np.int64)
+    if n:
+        np.cumsum(rec_words[:-1], out=rec_off[1:])
+    cap_offsets = np.zeros(n + 1, np.int64)
+    np.cumsum(caps, out=cap_offsets[1:])
+    records = torch.from_numpy(np.frombuffer(data, np.int32, (rec_end - rec0) // 4, rec0).copy()).to(dev)
+    walks = torch.empty((n, M, W), dtype=torch.int32, device=dev)
+    keys = torch.empty(int(cap_offsets[-1]), dtype=torch.int32, device=dev)
+    vals = torch.empty(int(cap_offsets[-1]), dtype=torch.int32, device=dev)
+    cap_d = torch.from_numpy(cap_offsets).to(dev)
+    _lib.call("wj_surl_unpack", _lib.ptr(records), n, MW, _lib.ptr(torch.from_numpy(rec_off).to(dev)),
+              _lib.ptr(cap_d), _lib.ptr(walks), _lib.ptr(keys), _lib.ptr(vals), _lib.stream_handle(dev))
+    del records
+    store = store_from_walks(walks, n, M, L, int(seed), id_map=id_map)
+    if store.table.vectors.shape != table.shape or not np.array_equal(store.table.vectors, table):
+        raise StoreFormatError("store file table is not the one its walks produce")
+    ref_caps, _, k2, v2 = store.export_dicts_device()
+    if not (np.array_equal(ref_caps, cap_offsets) and torch.equal(k2, keys) and torch.equal(v2, vals)):
+        raise StoreFormatError("store file dicts are not the ones its walks produce")
+    return store

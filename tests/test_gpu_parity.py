@@ -581,3 +581,39 @@ def test_join_cross_matches_sorted_lookup(wj, arity):
                 pc = np.minimum(pos, len(xj) - 1)
                 want = np.where((pos < len(xj)) & (xj[pc] == xa), ij[pc], 0)
                 np.testing.assert_array_equal(cross[b, a, jj, :len(xa)], want)
+
+
+@pytest.mark.parametrize("name", ["er200", "idmap120"])
+def test_save_store_is_byte_identical_to_reference(wj, name, tmp_path):
+    """save_store of the device store == the file the reference save_store
+    wrote for the same graph and arguments (tests/golden/make_surl_golden.py);
+    load_store of that file gives back the same walks, table and dicts."""
+    import os
+
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    d = np.load(os.path.join(here, f"surl_{name}.npz"))
+    ref = open(os.path.join(here, f"surl_{name}.surl"), "rb").read()
+    id_map = {int(k): int(v) for k, v in zip(d["id_keys"], d["id_vals"])} if len(d["id_keys"]) else None
+    g = wj.Graph(int(d["n"]), d["idxptr"], d["indices"], id_map=id_map)
+    s = wj.preprocess(g, int(d["M"]), int(d["L"]), int(d["seed"]))
+    out = tmp_path / "store.surl"
+    wj.save_store(s, out, chunk_bytes=4096)  # several device chunks
+    assert out.read_bytes() == ref
+    t = wj.load_store(out)
+    assert np.array_equal(t.walks, s.walks) and np.array_equal(t.table.vectors, s.table.vectors)
+    assert np.array_equal(t.dict_keys, s.dict_keys) and np.array_equal(t.dict_vals, s.dict_vals)
+    assert t.seed == s.seed and t.id_map == s.id_map
+
+
+def test_load_store_rejects_bad_files(wj, tmp_path):
+    import os
+
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    ref = open(os.path.join(here, "surl_er200.surl"), "rb").read()
+    cases = {"magic": b"XURL" + ref[4:], "truncated": ref[:-7], "trailing": ref + b"\0\0\0\0",
+             "version": ref[:4] + b"\x02" + ref[5:]}
+    for k, blob in cases.items():
+        p = tmp_path / f"{k}.surl"
+        p.write_bytes(blob)
+        with pytest.raises(wj.StoreFormatError):
+            wj.load_store(p)

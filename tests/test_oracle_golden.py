@@ -1,11 +1,15 @@
 """The CPU oracle reproduces the reference's own outputs (fixtures made by
 tests/golden/make_golden.py from the real reference)."""
 
+import os
+
 import numpy as np
 import pytest
 
 from conftest import golden_cases, load_golden
 from oracle import core, encoder_ref, pipeline_ref
+
+GOLDEN_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
 @pytest.mark.parametrize("name", golden_cases())
@@ -85,3 +89,16 @@ def test_minibatcher_matches_reference(golden_meta):
         negs = pipeline_ref.sample_negatives(seeds, 2, mb["k_neg"] * len(ids), pos_filter, rng)
         assert seeds == want["seeds"] and ids == want["ids"]
         assert [list(q) for q in negs] == want["negs"]
+
+
+@pytest.mark.parametrize("name", ["er200", "idmap120"])
+def test_oracle_surl_writer_matches_reference_file(name):
+    """The oracle's restatement of store._write_store reproduces the bytes
+    the reference save_store wrote (tests/golden/make_surl_golden.py)."""
+    from oracle import core
+
+    d = np.load(os.path.join(GOLDEN_DIR, f"surl_{name}.npz"))
+    ref = open(os.path.join(GOLDEN_DIR, f"surl_{name}.surl"), "rb").read()
+    s = core.preprocess(d["idxptr"], d["indices"], int(d["M"]), int(d["L"]), int(d["seed"]))
+    id_map = {int(k): int(v) for k, v in zip(d["id_keys"], d["id_vals"])} if len(d["id_keys"]) else None
+    assert core.write_surl(s, id_map) == ref
