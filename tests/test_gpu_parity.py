@@ -434,17 +434,16 @@ def _fused_model_mma(store, q, w1, b1, keep, seed, step):
 
 @pytest.mark.parametrize("keep", [1.0, 0.9])
 @pytest.mark.parametrize("kernel", ["mma", "simt"])
-def test_fused_join_encode_matches_host_model(wj, keep, kernel):
-    from paper_2202_13538_b200 import _lib
-
+@pytest.mark.parametrize("arity,L", [(2, 4), (3, 3)])
+def test_fused_join_encode_matches_host_model(wj, keep, kernel, arity, L):
     g = _er(800, 6_000, 4)
-    s = wj.preprocess(g, 40, 4, 21)
+    s = wj.preprocess(g, 40, L, 21)
     rng = np.random.default_rng(3)
-    q = np.stack([rng.choice(800, 2, replace=False) for _ in range(12)]).astype(np.int64)
-    p = wj.init_params(2, 4, dropout=1 - keep, seed=2)
+    q = np.stack([rng.choice(800, arity, replace=False) for _ in range(12)]).astype(np.int64)
+    p = wj.init_params(arity, L, dropout=1 - keep, seed=2)
     step = torch.tensor([6], dtype=torch.int64, device="cuda")
     pooled = torch.empty((12, 64), device="cuda")
-    S = torch.empty((12, 10, 64), device="cuda")
+    S = torch.empty((12, arity * (L + 1), 64), device="cuda")
     msum = torch.empty((12, 64), device="cuda")
     qd = torch.from_numpy(q).cuda()
     wj.encoder.join_encode(s, qd, p.w1, p.b1, float(keep), 99, step, pooled, S, msum, simt=(kernel == "simt"))
