@@ -293,29 +293,51 @@ def run_ours(args, cfg):
     e1.record()
     barrier_sync()
     t_pre_e2e = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+    # the batches come from the native planner (the reference's BFS batches +
+    # in-seed negatives on numpy's PCG64 stream, pipeline.py:287-305) on its
+    # producer thread, into pinned host slots: planning, H2D, step and the
+    # loss read-back are all inside the timed region; the planner's one-time
+    # build (query index + positive-tuple set, pipeline.py:276-280) is
+    # charged with the preprocess
+    from paper_2202_13538_b200.pipeline import BatchPlanner, TrainConfig
+
+    nn_ = cfg["n"]
+    filt_rows = np.stack([split.all_edges // nn_, split.all_edges % nn_], 1)
+    tp0 = time.perf_counter()
+    planner = BatchPlanner(split.train_pos, filt_rows, nn_, TrainConfig(batch_size=POS_PER_BATCH, k_neg=K_NEG),
+                           np.random.default_rng(BATCH_SEED + rank), depth=8)
+    t_plan_setup = max_over_ranks(time.perf_counter() - tp0)
+    del filt_rows
     params = wj.init_params(A, L, hidden=64, dropout=0.1, seed=11, device=dev)
     state = wj.AdamState.for_params(params, lr=1e-3)
     step = wj.TrainStep(store, params, state, dense_dtype=torch.float32, mode=args.mode,
                         use_graph=True, process_group=(dist.group.WORLD if world > 1 else None),
                         seed=1000 + rank, overlap_inputs=True)
-    qh =[torch.from_numpy(q).pin_memory() for q, _ in plan]
-    yh = [torch.from_numpy(y).pin_memory() for _, y in plan]
     loss_h = torch.empty(W + K, dtype=torch.float32).pin_memory()
+    it = planner.epoch()  # warm-up epoch: captures the step graphs, then abandoned
     for k in range(W):
-        loss_h[k:k + 1].copy_(step(qh[k], yh[k]).reshape(1), non_blocking=True)
-    for k in range(W, W + K):
-        if (qh[k].shape[0], A) not in step._graphs:
-            step(qh[k], yh[k])
+        q, y, _ = next(it)
+        loss_h[k:k + 1].copy_(step(q, y).reshape(1), non_blocking=True)
+        planner.release(step.input_event)
+    it.close()
     barrier_sync()
+    h2d_list = []
     w0 = time.perf_counter()
     e0.record()
+    it = planner.epoch()  # the producer thread starts inside the timed region
     for k in range(W, W + K):
-        loss_h[k:k + 1].copy_(step(qh[k], yh[k]).reshape(1), non_blocking=True)
+        q, y, _ = next(it)
+        loss_h[k:k + 1].copy_(step(q, y).reshape(1), non_blocking=True)
+        planner.release(step.input_event)
+        h2d_list.append(q.numel() * 8 + y.numel() * 4)
     e1.record()
     barrier_sync()
     wall = (time.perf_counter() - w0) / K
+    it.close()
+    planner.close()
     t_step_e2e = max_over_ranks(max(e0.elapsed_time(e1) / 1e3 / K, wall))
-    h2d = int(np.mean([qh[k].numel() * 8 + yh[k].numel() * 4 for k in range(W, W + K)]))
+    h2d = int(np.mean(h2d_list))
+    t_pre_e2e += t_plan_setup
 
     if args.mode == "fused" and step.fast_tail:
         launches_per_step = 3
@@ -406,7 +428,10 @@ def run_ours(args, cfg):
         },
         "e2e": {"value": round(e2e, 1), "unit": "queries/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": 4, "t_pre_ms": round(t_pre_e2e * 1e3, 3),
-                "ms_per_step": round(t_step_e2e * 1e3, 4)},
+                "t_planner_setup_ms": round(t_plan_setup * 1e3, 3),
+                "ms_per_step": round(t_step_e2e * 1e3, 4),
+                "path": ("host CSR -> preprocess; native batch planner (producer thread) -> pinned batch "
+                         "-> H2D -> step graph -> loss D2H, every step timed")},
         "roofline": roof,
         "gpu_launches": K * launches_per_step,
         "gpu_launches_note": launches_note,

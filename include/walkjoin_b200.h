@@ -243,6 +243,46 @@ int wj_surl_unpack(const int32_t *records, int64_t n_nodes, int32_t walk_words, 
 int wj_lookup(const int64_t *u, const int64_t *x, int64_t count, const int64_t *offsets,
               const int32_t *uniq_x, const int32_t *uniq_id, int32_t *out, wj_stream_t stream);
 
+
+/* ---- Host-side training mini-batch planner (no device state) -------------
+ * Replaces the per-batch Python of train() (pipeline.py:292-304):
+ * sample_minibatch (pipeline.py:77-129, BFS over query-sharing neighbours)
+ * and sample_negatives (pipeline.py:132-166, in-seed rejection negatives)
+ * or the fixed-pool draw (pipeline.py:298-300), on numpy's PCG64 stream:
+ * with the Generator state copied in (wj_planner_set_rng: state hi/lo,
+ * inc hi/lo, has_uint32, uinteger) each wj_planner_next returns exactly the
+ * reference's batch and leaves the same state (wj_planner_get_rng).
+ * The handle owns HOST memory (node -> query index, positive-tuple hash
+ * set); it is the one object in this ABI that allocates, and one handle
+ * must not be driven from two threads at once.  arity <= 4, node ids < 2^31.
+ * positives [n_pos, arity], filter_tuples [n_filter, arity] (the canonical
+ * positive set, pipeline.py:278-280), neg_pool [n_pool, arity] or NULL. */
+typedef struct wj_planner wj_planner;
+int wj_planner_create(const int64_t *positives, int64_t n_pos, int32_t arity, const int64_t *filter_tuples,
+                      int64_t n_filter, int64_t num_nodes, int32_t batch_capacity, int32_t batch_size,
+                      int32_t k_neg, const int64_t *neg_pool, int64_t n_pool, wj_planner **out);
+int wj_planner_destroy(wj_planner *planner);
+int wj_planner_set_rng(wj_planner *planner, const uint64_t *words6);
+int wj_planner_get_rng(const wj_planner *planner, uint64_t *words6);
+/* One batch: queries_out [cap, arity] (positives first, then negatives),
+ * labels_out [cap] (1 / 0, may be NULL); n_queries 0 = empty batch. */
+int wj_planner_next(wj_planner *planner, int64_t *queries_out, float *labels_out, int64_t cap,
+                    int64_t *n_queries_out, int64_t *n_pos_out, int64_t *n_seeds_out);
+/* One epoch of train()'s batch loop (pipeline.py:287-305) on a producer
+ * thread, ahead of the consumer: batches until the positives consumed reach
+ * n_pos or a batch is empty, written in order into a caller-owned ring of
+ * n_slots slots (ring_queries [n_slots, cap, arity], ring_labels
+ * [n_slots, cap], e.g. pinned host memory).  wj_planner_acquire spins until
+ * the next batch is ready and returns its slot (-1 at the end of the epoch,
+ * after which the rng state is the reference's end-of-epoch state);
+ * wj_planner_release hands a slot back once its contents have been copied.
+ * wj_planner_stop abandons the epoch (the rng state is then ahead). */
+int wj_planner_start_epoch(wj_planner *planner, int64_t *ring_queries, float *ring_labels, int32_t n_slots,
+                           int64_t cap);
+int wj_planner_acquire(wj_planner *planner, int32_t *slot_out, int64_t *n_queries_out, int64_t *n_pos_out);
+int wj_planner_release(wj_planner *planner, int32_t slot);
+int wj_planner_stop(wj_planner *planner);
+
 #ifdef __cplusplus
 }
 #endif

@@ -49,6 +49,15 @@ SIGNATURES = {
     "wj_lookup": [P, P, I64, P, P, P, P, P],
     "wj_surl_pack": [P, I64, I32, P, P, P, P, P, P],
     "wj_surl_unpack": [P, I64, I32, P, P, P, P, P, P],
+    "wj_planner_create": [P, I64, I32, P, I64, I64, I32, I32, I32, P, I64, P],
+    "wj_planner_destroy": [P],
+    "wj_planner_set_rng": [P, P],
+    "wj_planner_get_rng": [P, P],
+    "wj_planner_next": [P, P, P, I64, P, P, P],
+    "wj_planner_start_epoch": [P, P, P, I32, I64],
+    "wj_planner_acquire": [P, P, P, P],
+    "wj_planner_release": [P, I32],
+    "wj_planner_stop": [P],
 }
 
 _lib = None

@@ -14,7 +14,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "_walkjoin_b200.so")
 SOURCES = ["capi.cu", "sampler.cu", "rpe.cu", "intern.cu", "join.cu", "encode.cu", "encode_mma.cu", "tail.cu",
-           "vindex.cu", "surl.cu"]
+           "vindex.cu", "surl.cu", "planner.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-O3", "-std=c++17", "-lineinfo", "--use_fast_math",
@@ -47,7 +47,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     env = dict(os.environ)
 
     def compile_one(src):
-        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
         cmd = [NVCC, *compile_flags, "-c", "-I", os.path.join(ROOT, "include"), "-o", obj,
                os.path.join(CSRC, src)]
         if verbose:

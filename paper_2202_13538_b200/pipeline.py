@@ -202,6 +202,149 @@ def make_batch(index, positives: np.ndarray, pos_filter, cfg: TrainConfig, rng, 
     return q, labels
 
 
+def _rng_words(rng: np.random.Generator) -> np.ndarray:
+    s = rng.bit_generator.state
+    if s.get("bit_generator") != "PCG64":
+        raise NotImplementedError(f"the native planner restates numpy's PCG64, not {s.get('bit_generator')}")
+    m64 = (1 << 64) - 1
+    st, inc = int(s["state"]["state"]), int(s["state"]["inc"])
+    return np.array([st >> 64, st & m64, inc >> 64, inc & m64, int(s["has_uint32"]), int(s["uinteger"])],
+                    dtype=np.uint64)
+
+
+class BatchPlanner:
+    """Training batches from the native planner (csrc/planner.cpp,
+    ``wj_planner_*``): the reference's ``sample_minibatch`` +
+    ``sample_negatives`` (or the fixed negative pool) per batch
+    (pipeline.py:292-304) restated in C++ on the caller's numpy PCG64
+    generator, so the batches are the reference's own for the same seed and
+    ``rng`` ends in the state the reference would leave it in (after
+    ``sync()``).  Batches are written into a ring of pinned host buffers
+    (``depth`` deep; a buffer is reused only after the event recorded by the
+    consumer's copy of it has completed), ready for a non-blocking H2D.
+
+    ``next()`` -> (q [B, A] int64, y [B] float32, n_pos), views into the ring
+    (B = 0: empty batch)."""
+
+    def __init__(self, positives, filter_rows, num_nodes: int, cfg: TrainConfig, rng: np.random.Generator,
+                 pool=None, depth: int = 4, pinned: bool = True):
+        from . import _lib
+
+        pos = np.ascontiguousarray(positives, dtype=np.int64)
+        if pos.ndim != 2 or pos.shape[0] == 0:
+            raise ValueError("empty training query set")
+        filt = np.ascontiguousarray(filter_rows, dtype=np.int64).reshape(-1, pos.shape[1])
+        pl = None if pool is None or len(pool) == 0 else np.ascontiguousarray(pool, dtype=np.int64)
+        self._lib = _lib.load()
+        self.rng, self.arity = rng, int(pos.shape[1])
+        self.cap = int(cfg.batch_size) * (1 + int(cfg.k_neg))
+        h = ctypes.c_void_p()
+        _lib.call("wj_planner_create", pos.ctypes.data, pos.shape[0], self.arity, filt.ctypes.data,
+                  filt.shape[0], int(num_nodes), int(cfg.batch_capacity), int(cfg.batch_size), int(cfg.k_neg),
+                  None if pl is None else pl.ctypes.data, 0 if pl is None else pl.shape[0], ctypes.byref(h))
+        self._h = h
+        self._words = _rng_words(rng)
+        _lib.call("wj_planner_set_rng", self._h, self._words.ctypes.data)
+        mk = (lambda t: t.pin_memory()) if pinned and torch.cuda.is_available() else (lambda t: t)
+        self.depth = int(depth)
+        self._q = mk(torch.empty((self.depth, self.cap, self.arity), dtype=torch.int64))
+        self._y = mk(torch.empty((self.depth, self.cap), dtype=torch.float32))
+        self._ev = [None] * self.depth
+        self._i = 0
+        self._cur = 0
+        self._running = False
+        self._out = (ctypes.c_int64 * 3)()
+
+    def next(self):
+        """One batch, planned on the calling thread."""
+        from . import _lib
+
+        i = self._i
+        self._i = (i + 1) % self.depth
+        if self._ev[i] is not None:  # the copy that last read this buffer
+            self._ev[i].synchronize()
+            self._ev[i] = None
+        o = self._out
+        _lib.call("wj_planner_next", self._h, self._q[i].data_ptr(), self._y[i].data_ptr(), self.cap,
+                  ctypes.byref(o, 0), ctypes.byref(o, 8), ctypes.byref(o, 16))
+        B = int(o[0])
+        self._cur = i
+        return self._q[i][:B], self._y[i][:B], int(o[1])
+
+    def release(self, event) -> None:
+        """The last batch's buffers are read by work ``event`` completes
+        (e.g. the step's H2D copy); the slot is reused only after it."""
+        self._ev[self._cur] = event
+
+    def epoch(self):
+        """One epoch of train()'s batch loop (pipeline.py:287-305), planned
+        ahead on the native producer thread (``wj_planner_start_epoch``).
+        Yields (q, y, n_pos) views into the pinned ring; call ``release`` with
+        the event of the batch's copy before asking for the next one (no
+        event: the batch was consumed synchronously).  After a completed
+        epoch the rng is in the reference's end-of-epoch state."""
+        from . import _lib
+
+        _lib.call("wj_planner_start_epoch", self._h, self._q.data_ptr(), self._y.data_ptr(), self.depth,
+                  self.cap)
+        self._running = True
+        pending = deque()
+        slot = ctypes.c_int32()
+        o = self._out
+        try:
+            while True:
+                # hand back the slots whose copies have completed; keep at
+                # most depth-1 outstanding so the producer can always advance
+                while pending and (pending[0][1] is None or pending[0][1].query()):
+                    _lib.call("wj_planner_release", self._h, pending.popleft()[0])
+                while len(pending) >= self.depth - 1:
+                    s, ev = pending.popleft()
+                    if ev is not None:
+                        ev.synchronize()
+                    _lib.call("wj_planner_release", self._h, s)
+                _lib.call("wj_planner_acquire", self._h, ctypes.byref(slot), ctypes.byref(o, 0), ctypes.byref(o, 8))
+                s = int(slot.value)
+                if s < 0:
+                    self._running = False
+                    return
+                B = int(o[0])
+                self._cur = s
+                self._ev[s] = None
+                yield self._q[s][:B], self._y[s][:B], int(o[1])
+                pending.append((s, self._ev[s]))
+                self._ev[s] = None
+        finally:
+            if self._running:
+                self._lib.wj_planner_stop(self._h)
+                self._running = False
+
+    def sync(self) -> None:
+        """Write the planner's PCG64 state back into the numpy generator."""
+        from . import _lib
+
+        _lib.call("wj_planner_get_rng", self._h, self._words.ctypes.data)
+        w = [int(x) for x in self._words]
+        st = self.rng.bit_generator.state
+        st["state"] = {"state": (w[0] << 64) | w[1], "inc": (w[2] << 64) | w[3]}
+        st["has_uint32"], st["uinteger"] = w[4], w[5]
+        self.rng.bit_generator.state = st
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            if not self._running:
+                self.sync()
+            self._lib.wj_planner_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None) is not None and self._h.value:
+                self._lib.wj_planner_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
 class TrainStep:
     """One training step on the device, captured as CUDA graphs per batch
     shape (``use_graph``; two graphs with their own input buffers, so the
@@ -337,8 +480,10 @@ class TrainStep:
         B, A = q.shape
         self._prepare_bc()
         if not self.use_graph:
-            out = self._body(q.to(self.dev, non_blocking=True), y.to(self.dev, self.params.w1.dtype),
-                             self._buffers(B, A), self.inv_bc)
+            qd, yd = q.to(self.dev, non_blocking=True), y.to(self.dev, self.params.w1.dtype, non_blocking=True)
+            self.input_event = torch.cuda.Event()
+            self.input_event.record()
+            out = self._body(qd, yd, self._buffers(B, A), self.inv_bc)
             self.params.version += 1
             return out
         key = (B, A)
@@ -366,6 +511,7 @@ class TrainStep:
             if t.device.type == "cuda":
                 t.record_stream(cs)
         cur.wait_event(g["ready"])
+        self.input_event = g["ready"]  # completes once q / y have been read
         g["graph"].replay()
         g["done"].record(cur)
         self.params.version += 1
@@ -464,16 +610,19 @@ def validation_metric(store: SubgraphStore, params: E.ModelParams, split, cfg: T
 
 
 def train(store: SubgraphStore, split, cfg: TrainConfig, features=None, train_negatives=None,
-          use_graph: bool = True, exact_batches: bool = False):
+          use_graph: bool = True, exact_batches: bool = False, native_planner: bool = True):
     """Mini-batched training with early stopping (pipeline.py:241-326), same
     seeds, batch contract and history; every step runs on the device
     (``TrainStep``).  Returns (best params, history).
 
-    ``exact_batches=True`` draws the BFS seed nodes with the reference's
-    ``rng.choice`` (a permutation per batch), so with the same seed every
-    batch -- positives, negatives, labels -- is the reference's own; with
-    dropout off the trajectory then differs from the reference only by fp32
-    vs fp64 rounding."""
+    Batches come from the native planner (``BatchPlanner``, arity <= 4): a
+    producer thread that restates the reference's batch draws on the same
+    numpy PCG64 stream, so with the same seed every batch -- positives,
+    negatives, labels -- is the reference's own, and with dropout off the
+    trajectory differs from the reference only by fp32 vs fp64 rounding.
+    ``native_planner=False`` plans in Python: ``exact_batches=True`` then
+    draws the BFS seeds with the reference's ``rng.choice`` (exact), the
+    default by rejection (same distribution, different draws)."""
     from .seeds import derive_seed
 
     positives = _rows(split.train_pos)
@@ -502,13 +651,21 @@ def train(store: SubgraphStore, split, cfg: TrainConfig, features=None, train_ne
     feats_d = None if features is None else torch.as_tensor(features, dtype=torch.float32, device=dev)
     step = TrainStep(store, params, state, mode="fused" if feats_d is None else "pooled",
                      use_graph=use_graph, seed=derive_seed(cfg.seed, "dropout"), features=feats_d)
+    planner = None
+    if native_planner and arity <= 4:
+        planner = BatchPlanner(positives, np.concatenate(filt_rows), store.num_nodes, cfg, batch_rng, pool=pool)
     history = []
     best_params, best_metric, best_epoch = params.copy(), -np.inf, 0
     for epoch in range(1, cfg.max_epochs + 1):
         t0 = time.perf_counter()
         consumed, n_steps = 0, 0
         loss_sum = torch.zeros((), dtype=torch.float64, device=dev)
-        while consumed < positives.shape[0]:
+        if planner is not None:  # native planner, producer thread ahead of the device
+            for q, y, _ in planner.epoch():
+                loss_sum += step(q, y).double()
+                planner.release(step.input_event)
+                n_steps += 1
+        while planner is None and consumed < positives.shape[0]:
             seeds, ids = sample_minibatch(index, positives, cfg, batch_rng, exact=exact_batches)
             if not ids:
                 break
@@ -532,6 +689,8 @@ def train(store: SubgraphStore, split, cfg: TrainConfig, features=None, train_ne
             best_metric, best_params, best_epoch = valid, params.copy(), epoch
         if epoch - best_epoch >= cfg.patience:
             break
+    if planner is not None:
+        planner.close()  # the generator ends in the reference's state
     return best_params, history
 
 
