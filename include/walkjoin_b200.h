@@ -52,6 +52,30 @@ int wj_sample_walks(const void *idxptr, int idxptr_bytes, const int32_t *indices
                     int64_t lo, int64_t hi, int32_t num_walks, int32_t num_steps, uint64_t seed,
                     int32_t *walks_out, uint8_t *fix_flags, wj_stream_t stream);
 
+/* Typed / metapath walks (no reference implementation exists --
+ * SPEC.md:121-124 leaves typed walks open -- so the semantics are ours,
+ * chosen so that the homogeneous special case IS wj_sample_walks): step i
+ * of walk j from anchor u follows an edge of type metapath[(i-1) % P]
+ * (negative = any edge), uniform among the current node's edges of that type
+ * in CSR order, with the reference's draw mix64(S0(u) + (j*L+i)*G); with no
+ * such edge the walk stays put for that step.  metapath is a HOST array of
+ * P <= 32 entries (copied into the launch); type_off [n*T+1] int64 /
+ * typed_indices [2E] int32 come from the grouping below (NULL allowed when every
+ * entry is negative).  With metapath {-1} on the reference's symmetric CSR
+ * the walks equal wj_sample_walks bit for bit. */
+int wj_sample_walks_typed(const void *idxptr, int idxptr_bytes, const int32_t *indices, const int64_t *type_off,
+                          const int32_t *typed_indices, int32_t num_types, const int8_t *metapath,
+                          int32_t metapath_len, int64_t n_nodes, int64_t lo, int64_t hi, int32_t num_walks,
+                          int32_t num_steps, uint64_t seed, int32_t *walks_out, wj_stream_t stream);
+
+/* Edge-type grouping of a CSR for the typed sampler: typed_indices_out [2E]
+ * = each node's neighbours grouped by edge type (edge_types [2E] uint8,
+ * aligned with indices; CSR order kept inside a type), type_off_out
+ * [n*T + 1] = start of node c's type-t group.  1 <= num_types <= 64. */
+int wj_typed_csr(const void *idxptr, int idxptr_bytes, const int32_t *indices, const uint8_t *edge_types,
+                 int64_t n_nodes, int32_t num_types, int64_t *type_off_out, int32_t *typed_indices_out,
+                 wj_stream_t stream);
+
 /* One anchor from an explicit stream state; writes the end state.
  * Replaces _kernels.sample_node_walks (_kernels.py:53-66) as used by
  * sampler.sample_walks (sampler.py:61-76). */

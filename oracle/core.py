@@ -53,6 +53,7 @@ def lib():
         L.wjo_dict_get_one.restype = ctypes.c_int32
         L.wjo_join_fill.argtypes = [P, I64, I64, P, P, P, P, I64, I64, P, P, I]
         L.wjo_densify.argtypes = [P, I64, P, I64, P, I]
+        L.wjo_sample_typed.argtypes = [P, P, P, P, I64, I64, I64, I64, U64, P, I]
         _lib = L
     return _lib
 
@@ -104,6 +105,20 @@ def sample_nodes(idxptr, indices, nodes, num_walks, num_steps, seed, threads=Non
     walks = np.empty((nodes.shape[0], num_walks, num_steps + 1), np.int32)
     lib().wjo_sample_nodes(_p(idxptr), _p(indices), _p(nodes), nodes.shape[0], num_walks,
                            num_steps, int(seed) & _MASK64, _p(walks), threads or default_threads())
+    return walks
+
+
+def sample_typed_walks(idxptr, indices, edge_types, metapath, num_walks, num_steps, seed, threads=None):
+    """Typed / metapath walks (our definition, no reference
+    implementation -- see walkjoin_oracle.c wjo_sample_typed)."""
+    idxptr = np.ascontiguousarray(idxptr, np.int64)
+    indices = np.ascontiguousarray(indices, np.int32)
+    et = np.ascontiguousarray(edge_types, np.uint8)
+    mp = np.ascontiguousarray(metapath, np.int8)
+    n = idxptr.shape[0] - 1
+    walks = np.empty((n, num_walks, num_steps + 1), np.int32)
+    lib().wjo_sample_typed(_p(idxptr), _p(indices), _p(et), _p(mp), mp.shape[0], n, num_walks, num_steps,
+                           int(seed) & _MASK64, _p(walks), threads or default_threads())
     return walks
 
 

@@ -283,3 +283,47 @@ void wjo_densify(const int32_t *table, int64_t width, const int32_t *rpe_ids, in
         for (int64_t c = 0; c < width; ++c) out[t * width + c] = (double)v[c];
     }
 }
+
+/* Typed / metapath walks.  NO reference implementation exists
+ * (SPEC.md:121-124 leaves typed walks open), so this restates OUR definition
+ * (include/walkjoin_b200.h, wj_sample_walks_typed) straight from the CSR and
+ * the per-entry edge types, without the device's type-grouped layout: step i
+ * of walk j from u follows an edge of type metapath[(i-1) % P] (negative =
+ * any), the idx-th such edge of the current node in CSR order with
+ * idx = umulhi32(mix64(S0(u) + (j*L+i)*G), count); none -> stay.  Its
+ * homogeneous special case is pinned to the reference sampler (K:53-74) by
+ * tests/test_typed_walks.py; the typed semantics are "parity unpinned". */
+void wjo_sample_typed(const int64_t *idxptr, const int32_t *indices, const uint8_t *etype,
+                      const int8_t *metapath, int64_t P, int64_t n, int64_t num_walks,
+                      int64_t num_steps, uint64_t seed, int32_t *walks, int threads) {
+    set_threads(threads);
+    const int64_t width = num_steps + 1;
+#pragma omp parallel for schedule(dynamic, 256)
+    for (int64_t u = 0; u < n; ++u) {
+        const uint64_t s0 = wjo_node_stream_state(seed, u);
+        int32_t *out = walks + u * num_walks * width;
+        for (int64_t j = 0; j < num_walks; ++j) {
+            int64_t cur = u;
+            out[j * width] = (int32_t)cur;
+            for (int64_t i = 1; i <= num_steps; ++i) {
+                const int t = metapath[(i - 1) % P];
+                int64_t cnt = 0;
+                for (int64_t e = idxptr[cur]; e < idxptr[cur + 1]; ++e) cnt += (t < 0 || etype[e] == t);
+                if (cnt > 0) {
+                    const uint64_t z = mix64(s0 + (uint64_t)(j * num_steps + i) * WJ_GOLDEN);
+                    int64_t k = (int64_t)(((z >> 32) * (uint64_t)cnt) >> 32);
+                    for (int64_t e = idxptr[cur]; e < idxptr[cur + 1]; ++e) {
+                        if (t < 0 || etype[e] == t) {
+                            if (k == 0) {
+                                cur = indices[e];
+                                break;
+                            }
+                            --k;
+                        }
+                    }
+                }
+                out[j * width + i] = (int32_t)cur;
+            }
+        }
+    }
+}

@@ -27,6 +27,8 @@ U64 = ctypes.c_uint64
 SIGNATURES = {
     "wj_sample_walks": [P, ctypes.c_int, P, I64, I64, I64, I32, I32, U64, P, P, P],
     "wj_sample_node_walks": [P, ctypes.c_int, P, I64, I32, I32, U64, P, P, P],
+    "wj_sample_walks_typed": [P, ctypes.c_int, P, P, P, I32, P, I32, I64, I64, I64, I32, I32, U64, P, P],
+    "wj_typed_csr": [P, ctypes.c_int, P, P, I64, I32, P, P, P],
     "wj_rpe_count": [P, I64, I32, I32, I64, P, P],
     "wj_rpe_fill": [P, I64, I32, I32, I64, P, P, P, P, P, P],
     "wj_intern_insert": [P, P, P, I64, I64, P, P, I64, P, P],

@@ -216,3 +216,89 @@ def store_from_walks(walks: torch.Tensor, n: int, M: int, L: int, seed64: int, i
     if keep_keys:
         store.uniq_key_d = ukey
     return store
+
+
+# ------------------------------------------------------ typed / metapath walks
+# SURVEY C4.  The reference has no typed sampler (SPEC.md:121-124 leaves it
+# open); the semantics are defined in include/walkjoin_b200.h
+# (wj_sample_walks_typed) so that metapath [-1] -- or a single edge type -- is
+# exactly the reference sampler.
+
+@dataclass
+class TypedCSR:
+    """Edge-type grouping of a device CSR (wj_typed_csr)."""
+
+    num_types: int
+    type_off: torch.Tensor       # [n*T + 1] int64
+    typed_indices: torch.Tensor  # [2E] int32
+
+
+def edge_types_from_node_types(g, node_types, num_node_types: int) -> np.ndarray:
+    """Per-CSR-entry relation type of a heterogeneous graph: the edge from a
+    type-a node to a type-b node gets type a*K + b (K = num_node_types), so a
+    metapath is a sequence of (from, to) node-type pairs."""
+    nt = np.asarray(node_types, dtype=np.int64)
+    K = int(num_node_types)
+    if nt.shape[0] != g.num_nodes or (nt.size and (nt.min() < 0 or nt.max() >= K)):
+        raise ValueError("node_types must give a type in [0, num_node_types) for every node")
+    if K * K > 64:
+        raise ValueError("at most 8 node types (64 relation types)")
+    idxptr = np.asarray(g.idxptr if not isinstance(g.idxptr, torch.Tensor) else g.idxptr.cpu().numpy(), np.int64)
+    indices = np.asarray(g.indices if not isinstance(g.indices, torch.Tensor) else g.indices.cpu().numpy(), np.int64)
+    rows = np.repeat(np.arange(g.num_nodes, dtype=np.int64), np.diff(idxptr))
+    return (nt[rows] * K + nt[indices]).astype(np.uint8)
+
+
+def typed_csr(g, edge_types, num_types: int = None, device=None) -> TypedCSR:
+    """Group every node's neighbours by edge type on the device (stable)."""
+    dev = _lib.require_cuda(device if device is not None else getattr(g, "device", None))
+    dg = DeviceGraph.from_graph(g, dev)
+    et = torch.as_tensor(np.asarray(edge_types, dtype=np.uint8) if not isinstance(edge_types, torch.Tensor)
+                         else edge_types).to(dev, torch.uint8)
+    if et.numel() != dg.indices.numel():
+        raise ValueError(f"edge_types has {et.numel()} entries for {dg.indices.numel()} CSR entries")
+    T = int(num_types) if num_types is not None else (int(et.max().item()) + 1 if et.numel() else 1)
+    type_off = torch.empty(dg.num_nodes * T + 1, dtype=torch.int64, device=dev)
+    if dg.num_nodes == 0:
+        type_off.zero_()
+    typed = torch.empty_like(dg.indices)
+    _lib.call("wj_typed_csr", _lib.ptr(dg.idxptr), dg.idxptr_bytes, _lib.ptr(dg.indices), _lib.ptr(et),
+              dg.num_nodes, T, _lib.ptr(type_off), _lib.ptr(typed), _lib.stream_handle(dev))
+    return TypedCSR(T, type_off, typed)
+
+
+def sample_walks_typed(g, tcsr: TypedCSR, metapath, num_walks: int, num_steps: int, seed: int,
+                       lo: int = 0, hi: int = None, device=None) -> torch.Tensor:
+    """Metapath walks of anchors [lo, hi) -> device int32 [hi-lo, M, L+1]."""
+    if num_walks < 1 or num_steps < 1:
+        raise ValueError("num_walks and num_steps must be >= 1")
+    mp = np.ascontiguousarray(metapath, dtype=np.int8)
+    if mp.ndim != 1 or not 1 <= mp.shape[0] <= 32:
+        raise ValueError("metapath must be a sequence of 1..32 edge types (negative = any edge)")
+    dev = _lib.require_cuda(device if device is not None else getattr(g, "device", None))
+    dg = DeviceGraph.from_graph(g, dev)
+    hi = dg.num_nodes if hi is None else int(hi)
+    walks = torch.empty((hi - lo, num_walks, num_steps + 1), dtype=torch.int32, device=dev)
+    T = 0 if tcsr is None else tcsr.num_types
+    _lib.call("wj_sample_walks_typed", _lib.ptr(dg.idxptr), dg.idxptr_bytes, _lib.ptr(dg.indices),
+              None if tcsr is None else _lib.ptr(tcsr.type_off),
+              None if tcsr is None else _lib.ptr(tcsr.typed_indices), T, mp.ctypes.data, mp.shape[0],
+              dg.num_nodes, int(lo), hi, int(num_walks), int(num_steps), _u64(seed), _lib.ptr(walks),
+              _lib.stream_handle(dev))
+    return walks
+
+
+def preprocess_typed(g, edge_types, metapath, num_walks: int, num_steps: int, seed: int, num_types: int = None,
+                     device=None, keep_keys: bool = False) -> SubgraphStore:
+    """Alg. 1 with metapath walks: typed sampling, then the same RPE /
+    interning / index phases as ``preprocess``; the store joins, encodes and
+    exports like any other."""
+    if g.num_nodes >= 2 ** 31:
+        raise ValueError("graphs with >= 2^31 nodes are not supported")
+    dev = _lib.require_cuda(device if device is not None else getattr(g, "device", None))
+    mp = np.ascontiguousarray(metapath, dtype=np.int8)
+    tcsr = typed_csr(g, edge_types, num_types, dev) if (mp >= 0).any() else None
+    walks = sample_walks_typed(g, tcsr, mp, num_walks, num_steps, seed, device=dev)
+    del tcsr
+    return store_from_walks(walks, int(g.num_nodes), int(num_walks), int(num_steps), _u64(seed),
+                            id_map=getattr(g, "id_map", None), keep_keys=keep_keys)
