@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--cpu-shard-nodes", type=int, default=0, help="0 = auto")
+    ap.add_argument("--launch", default="chain", choices=["chain", "graph"],
+                    help="chain: native step executor, PDL-chained across steps; graph: one CUDA graph per step")
     ap.add_argument("--mode", default="fused", choices=["fused", "pooled", "reference"],
                     help="fused: wj_join_encode kernel; pooled/reference: wj_join dense + PyTorch encoder")
     return ap.parse_args()
@@ -222,11 +224,11 @@ def run_ours(args, cfg):
     state = wj.AdamState.for_params(params, lr=1e-3)
     step = wj.TrainStep(store, params, state, dense_dtype=torch.float32, mode=args.mode,
                         use_graph=True, process_group=(dist.group.WORLD if world > 1 else None),
-                        seed=1000 + rank, overlap_inputs=True)
+                        seed=1000 + rank, overlap_inputs=True, launch=args.launch)
     for k in range(W):                       # warm-up: captures every batch shape of the plan
         step(qd[k], yd[k])
     for k in range(W, W + K):
-        if (qd[k].shape[0], A) not in step._graphs:
+        if step.launch == "graph" and (qd[k].shape[0], A) not in step._graphs:
             step(qd[k], yd[k])
 
     # ---- value: K steps, inputs resident in HBM
@@ -312,13 +314,21 @@ def run_ours(args, cfg):
     state = wj.AdamState.for_params(params, lr=1e-3)
     step = wj.TrainStep(store, params, state, dense_dtype=torch.float32, mode=args.mode,
                         use_graph=True, process_group=(dist.group.WORLD if world > 1 else None),
-                        seed=1000 + rank, overlap_inputs=True)
+                        seed=1000 + rank, overlap_inputs=True, launch=args.launch)
     loss_h = torch.empty(W + K, dtype=torch.float32).pin_memory()
     it = planner.epoch()  # warm-up epoch: captures the step graphs, then abandoned
+    chain = step.launch == "chain"
+
+    def e2e_step(k, q, y):
+        if chain:  # the Adam kernel writes the loss straight into pinned host memory
+            step(q, y, loss_out=loss_h[k:k + 1])
+        else:
+            loss_h[k:k + 1].copy_(step(q, y).reshape(1), non_blocking=True)
+        planner.release(step.input_event)
+
     for k in range(W):
         q, y, _ = next(it)
-        loss_h[k:k + 1].copy_(step(q, y).reshape(1), non_blocking=True)
-        planner.release(step.input_event)
+        e2e_step(k, q, y)
     it.close()
     barrier_sync()
     h2d_list = []
@@ -327,8 +337,7 @@ def run_ours(args, cfg):
     it = planner.epoch()  # the producer thread starts inside the timed region
     for k in range(W, W + K):
         q, y, _ = next(it)
-        loss_h[k:k + 1].copy_(step(q, y).reshape(1), non_blocking=True)
-        planner.release(step.input_event)
+        e2e_step(k, q, y)
         h2d_list.append(q.numel() * 8 + y.numel() * 4)
     e1.record()
     barrier_sync()
@@ -341,7 +350,9 @@ def run_ours(args, cfg):
 
     if args.mode == "fused" and step.fast_tail:
         launches_per_step = 3
-        launches_note = ("per timed step (one CUDA graph, PDL-chained): wj_join_encode (join + layer 1), "
+        launches_note = (("per timed step (native step executor, one PDL chain across steps): "
+                          if step.launch == "chain" else "per timed step (one CUDA graph, PDL-chained): ") +
+                         "wj_join_encode (join + layer 1), "
                          "wj_encoder_tail (tensor-core tail + partial grads), wj_adam")
     else:
         launches_per_step = 1
@@ -438,6 +449,7 @@ def run_ours(args, cfg):
             "l2": "inputs larger than L2 (store > 40 GB, a different random batch every step)",
             "final_loss": final_loss,
             "parallelism": f"dp{world}",
+            "launch": step.launch,
         },
         "e2e": {"value": round(e2e, 1), "unit": "queries/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": 4, "t_pre_ms": round(t_pre_e2e * 1e3, 3),

@@ -227,6 +227,32 @@ int wj_adam(float *params, float *m, float *v, const float *partial, int32_t par
             int32_t n_params, float lr, float beta1, float beta2, float eps, const int64_t *step,
             float *grad_out, float *loss_out, wj_stream_t stream);
 
+/* Step executor: one fused training step per wj_stepper_run --
+ * wj_join_encode -> wj_encoder_tail -> wj_adam with every static argument
+ * (the store's index, flat params / Adam moments at offsets9, work buffers
+ * pooled [B_max, 64], s_out [B_max, A*(L+1), 64], msum [B_max, 64],
+ * partial [partial_rows_max, n_params + 1], the device step counter,
+ * tail_scale = 1 / (keep_prob * A * M * (L+1)) as wj_encoder_tail takes it) fixed
+ * at creation.  All three launches are programmatic-dependent, so
+ * consecutive runs on one stream form a single PDL chain: the next step's
+ * join+encode kernel stages its first query while this step's tail and Adam
+ * finish.  queries [B, A] int64 / labels [B] fp32 may be device memory or
+ * mapped pinned host memory (read by the kernels directly; the caller keeps
+ * them unchanged until the step completes); loss_out (device or mapped
+ * host, may be NULL) receives the step's mean BCE.  Same math and dropout
+ * stream as the three separate calls (the TrainStep graph). */
+typedef struct wj_stepper wj_stepper;
+int wj_stepper_create(const int64_t *offsets, const int32_t *uniq_x, const int32_t *uniq_id, const int64_t *voff,
+                      const int32_t *vcnt, const uint16_t *vslots, const uint16_t *table_rows_f16, int32_t arity,
+                      int32_t num_walks, int32_t num_steps, int32_t max_unique, float *params, float *adam_m,
+                      float *adam_v, const int32_t *offsets9, float keep_prob, float tail_scale, uint64_t seed,
+                      float lr, float beta1,
+                      float beta2, float eps, int64_t *step, float *pooled, float *s_out, float *msum,
+                      float *partial, int32_t partial_rows_max, wj_stepper **out);
+int wj_stepper_run(wj_stepper *stepper, const int64_t *queries, const float *labels, int64_t n_batch,
+                   float *loss_out, wj_stream_t stream);
+int wj_stepper_destroy(wj_stepper *stepper);
+
 /* Fixed-order column sums out[c] = sum_r partial[r, c] of a [rows, n_cols]
  * partial buffer (the data-parallel step reduces locally, all-reduces the
  * [n_params + 1] result over ranks, then runs wj_adam on it as one row). */

@@ -37,6 +37,7 @@
 #include <cuda_fp16.h>
 
 #include <cstdlib>
+#include <new>
 
 #include "common.cuh"
 
@@ -52,7 +53,7 @@ struct QMeta {
     int64_t lo, vo;  // first entry of the anchor's sorted list / of its virtual landings
     int u, v2, v1;   // list length, 2-row and 1-row virtual landings
 };
-constexpr int kHdrBytes = (kMetaQ * 3 * (int)sizeof(QMeta) + 16 + 15) & ~15;
+constexpr int kHdrBytes = (kMetaQ * 3 * (int)sizeof(QMeta) + 16 + 32 + 15) & ~15;  // meta | wscale[4] | wred[8]
 
 struct EncMmaArgs {
     const int64_t *queries;
@@ -332,11 +333,11 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
         }
     };
     load_meta(blockIdx.x);
-    pdl_wait();  // params / step counter come from the previous kernel in the stream
-    const uint64_t skey = mix64(g.seed + kGolden * ((uint64_t)(g.step ? *g.step : 0) + 1ULL));
+    __syncthreads();
+    float *wred = wscale + 4;  // [kMW] W^T max-reduction scratch (the rows area is live by then)
 
     // ---- W^T = [W1; b1; 0]^T as a power-of-two-scaled fp16 hi + lo pair
-    {
+    auto stage_wt = [&]() {
         float mx = 0.f;
         for (int i = threadIdx.x; i < (AW + 1) * H; i += NT) {
             const float w = i < AW * H ? g.w1[i] : g.b1[i - AW * H];
@@ -344,11 +345,11 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
         }
 #pragma unroll
         for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
-        if (lane == 0) red[warp] = mx;
+        if (lane == 0) wred[warp] = mx;
         __syncthreads();
         if (threadIdx.x == 0) {
             float m = 0.f;
-            for (int w = 0; w < kMW; ++w) m = fmaxf(m, red[w]);
+            for (int w = 0; w < kMW; ++w) m = fmaxf(m, wred[w]);
             int e = 0;
             if (m > 0.f) frexpf(m, &e);  // m in [2^(e-1), 2^e)
             const int s = 14 - e;        // scaled max in [2^13, 2^14)
@@ -365,12 +366,11 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
             wt[H * kWS + m * kWS + k] = lo;
         }
         __syncthreads();
-    }
-
+    };
+    uint64_t skey = 0;
 
     int jq = 0;  // local query index
     for (int64_t b = blockIdx.x; b < g.n_batch; b += gridDim.x, ++jq) {
-        if (b + gridDim.x >= g.n_batch) pdl_trigger();  // last query of this CTA: dependents may launch
         if (jq > 0 && jq % kMetaQ == 0) {  // metadata of the CTA's next kMetaQ queries
             __syncthreads();
             load_meta(b);
@@ -424,6 +424,17 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
         }
         build_rows_x<A, W>(g, threadIdx.x, NT, scr, sid, pu, xr);
         __syncthreads();
+
+        if (jq == 0) {
+            // Everything above reads only the store and this step's queries,
+            // so under PDL it overlaps the previous step's tail and Adam; W1,
+            // b1 and the step counter are written by them: wait here.
+            pdl_wait();
+            skey = mix64(g.seed + kGolden * ((uint64_t)(g.step ? *g.step : 0) + 1ULL));
+            stage_wt();
+        }
+        // last query of this CTA, after the wait: dependents may launch
+        if (b + gridDim.x >= g.n_batch) pdl_trigger();
 
         // ---- per-warp tiles of 16 virtual landings
         uint32_t qq = (uint32_t)mix64(skey ^ mix64((uint64_t)b));
@@ -725,6 +736,114 @@ extern "C" int wj_join_encode(const int64_t *queries, int64_t n_batch, int32_t a
         return WJ_ERR_CUDA;
     }
     return check_launch("wj_join_encode");
+}
+
+
+// ---------------------------------------------------------------------------
+// Step executor: one fused training step (wj_join_encode -> wj_encoder_tail
+// -> wj_adam) per call, every launch programmatic-dependent, so consecutive
+// steps form one PDL chain on the stream: the next step's join+encode
+// kernel is launched as soon as this step's Adam kernel starts, and stages
+// its first query (lists, cross ids, rows) while the tail and Adam finish;
+// it waits (griddepcontrol.wait) only before it needs W1.  The static
+// arguments and the kernel plan are fixed at creation, so a step costs one
+// host call and three launches.  Inputs may live in mapped (pinned) host
+// memory: the queries are read before the wait, the labels are prefetched by
+// the tail before its wait.
+struct wj_stepper {
+    wj::MmaPlan plan;
+    wj::EncMmaArgs args;
+    int32_t arity, aw, tail_rows_max, n_params;
+    int32_t offsets9[9];
+    float *params, *m, *v, *partial;
+    int64_t *step;
+    float scale, lr, beta1, beta2, eps;
+};
+
+extern "C" int wj_stepper_create(const int64_t *offsets, const int32_t *uniq_x, const int32_t *uniq_id,
+                                 const int64_t *voff, const int32_t *vcnt, const uint16_t *vslots,
+                                 const uint16_t *table_rows_f16, int32_t arity, int32_t num_walks, int32_t num_steps,
+                                 int32_t max_unique, float *params, float *adam_m, float *adam_v,
+                                 const int32_t *offsets9, float keep_prob, float tail_scale, uint64_t seed, float lr, float beta1,
+                                 float beta2, float eps, int64_t *step, float *pooled, float *s_out, float *msum,
+                                 float *partial, int32_t partial_rows_max, wj_stepper **out) {
+    using namespace wj;
+    if (!out || !params || !adam_m || !adam_v || !offsets9 || !step || !pooled || !s_out || !msum || !partial ||
+        partial_rows_max < 1 || arity < 1 || num_walks < 1 || num_steps < 1 || !(keep_prob > 0.f) || keep_prob > 1.f) {
+        set_error("wj_stepper_create: bad arguments");
+        return WJ_ERR_ARG;
+    }
+    if (!voff || !vcnt || !vslots || !table_rows_f16) {
+        set_error("wj_stepper_create: the store's virtual-landing index and fp16 table rows are required");
+        return WJ_ERR_ARG;
+    }
+    wj_stepper *st = new (std::nothrow) wj_stepper();
+    if (!st) {
+        set_error("wj_stepper_create: out of host memory");
+        return WJ_ERR_ARG;
+    }
+    int rc = plan_mma(arity, num_walks, num_steps, max_unique, st->plan);
+    if (rc != WJ_OK || !st->plan.k) {
+        delete st;
+        if (rc == WJ_OK) set_error("wj_stepper_create: shape outside the tensor-core kernel");
+        return rc == WJ_OK ? WJ_ERR_UNSUPPORTED : rc;
+    }
+    fill_args(st->args, st->plan, nullptr, 0, offsets, uniq_x, uniq_id, voff, vcnt, vslots, table_rows_f16,
+              keep_prob, seed, step);
+    st->args.w1 = params + offsets9[0];
+    st->args.b1 = params + offsets9[1];
+    st->args.cross = nullptr;
+    st->args.pooled = pooled;
+    st->args.s_out = s_out;
+    st->args.msum = msum;
+    st->arity = arity;
+    st->aw = arity * (num_steps + 1);
+    st->tail_rows_max = partial_rows_max;
+    for (int i = 0; i < 9; ++i) st->offsets9[i] = offsets9[i];
+    st->n_params = offsets9[8];
+    st->params = params;
+    st->m = adam_m;
+    st->v = adam_v;
+    st->partial = partial;
+    st->step = step;
+    st->scale = tail_scale;
+    st->lr = lr;
+    st->beta1 = beta1;
+    st->beta2 = beta2;
+    st->eps = eps;
+    *out = st;
+    return WJ_OK;
+}
+
+extern "C" int wj_stepper_destroy(wj_stepper *st) {
+    delete st;
+    return WJ_OK;
+}
+
+extern "C" int wj_stepper_run(wj_stepper *st, const int64_t *queries, const float *labels, int64_t n_batch,
+                              float *loss_out, wj_stream_t stream) {
+    using namespace wj;
+    if (!st || !queries || !labels || n_batch < 1) {
+        set_error("wj_stepper_run: bad arguments");
+        return WJ_ERR_ARG;
+    }
+    EncMmaArgs g = st->args;
+    g.queries = queries;
+    g.n_batch = n_batch;
+    const int64_t blocks = n_batch < st->plan.slots ? n_batch : st->plan.slots;
+    cudaError_t e = launch_pdl(st->plan.k, dim3((unsigned)blocks), dim3(st->plan.nw * 32), st->plan.smem,
+                               (cudaStream_t)stream, g);
+    if (e != cudaSuccess) {
+        set_error("wj_stepper_run: join_encode launch: %s", cudaGetErrorString(e));
+        return WJ_ERR_CUDA;
+    }
+    int64_t rows = (n_batch + 15) / 16;
+    if (rows > st->tail_rows_max) rows = st->tail_rows_max;
+    int rc = wj_encoder_tail(g.pooled, g.s_out, g.msum, labels, n_batch, st->aw, 64, st->params, st->offsets9,
+                             st->scale, nullptr, st->partial, (int32_t)rows, nullptr, st->step, stream);
+    if (rc != WJ_OK) return rc;
+    return wj_adam(st->params, st->m, st->v, st->partial, (int32_t)rows, st->n_params, st->lr, st->beta1, st->beta2,
+                   st->eps, st->step, nullptr, loss_out, stream);
 }
 
 

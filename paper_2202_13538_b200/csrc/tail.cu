@@ -83,6 +83,9 @@ __global__ void __launch_bounds__(kAdamCols *kAdamGroups) adam_kernel(
     __shared__ float part[kAdamGroups][kAdamCols];
     const int c = threadIdx.x & (kAdamCols - 1), grp = threadIdx.x / kAdamCols;
     const int i = blockIdx.x * kAdamCols + c;
+    // the next step's join+encode kernel may launch now: before its own wait
+    // it only reads the store and its queries, which this kernel never writes
+    pdl_trigger();
     pdl_wait();  // the partial rows of the tail kernel
     float gsum = 0.f;
     if (i <= n) gsum = strided_sum(partial + i, (int64_t)(n + 1), grp, rows);
@@ -181,6 +184,7 @@ __device__ __forceinline__ void warp_mma3(float (&acc)[NT][4], int lane, LA la, 
 }
 
 constexpr int kTW = 8;  // warps per tail CTA
+constexpr int kTailLabels = 64;  // labels per CTA prefetched into shared memory
 
 template <int AW>
 __global__ void __launch_bounds__(kTW * 32) tail_tc_kernel(TailArgs g) {
@@ -199,11 +203,16 @@ __global__ void __launch_bounds__(kTW * 32) tail_tc_kernel(TailArgs g) {
         cp_async16(U1s + r * kTP + c, P + g.off.u1 + r * 64 + c);
     }
     const float u2a = P[g.off.u2 + lane], u2b = P[g.off.u2 + lane + 32], c2 = P[g.off.c2];
-    pdl_wait();     // pooled / S / msum of the join+encode kernel
-    pdl_trigger();  // the Adam kernel may get scheduled
     const bool train = g.labels != nullptr;
     const int64_t q_lo = (int64_t)blockIdx.x * g.per_cta;
     const int64_t q_hi = min(g.B, q_lo + g.per_cta);
+    // this CTA's labels (inputs, possibly in mapped host memory): fetched
+    // before the wait so their latency overlaps the join+encode kernel
+    float *LB = SS + kTQ * (AW + 1) * 64;  // [kTailLabels]
+    if (train)
+        for (int64_t i = tid; i < min((int64_t)kTailLabels, q_hi - q_lo); i += NT) LB[i] = g.labels[q_lo + i];
+    pdl_wait();     // pooled / S / msum of the join+encode kernel
+    pdl_trigger();  // the Adam kernel may get scheduled
     constexpr int NW1 = ((AW + 1) * 64 + NT - 1) / NT;
     // dW2 / dU1 tiles of this warp: m-tile (warp & 3), n-tiles 4 (warp >> 2) .. +3
     const int fm = warp & 3, fn = (warp >> 2) * 4;
@@ -264,7 +273,8 @@ __global__ void __launch_bounds__(kTW * 32) tail_tc_kernel(TailArgs g) {
             if (q < nq) {
                 if (g.logits && lane == 0) g.logits[q0 + q] = z;
                 if (train) {
-                    const float y = g.labels[q0 + q];
+                    const int64_t li = q0 + q - q_lo;
+                    const float y = li < kTailLabels ? LB[li] : g.labels[q0 + q];
                     const float sig = z >= 0.f ? 1.f / (1.f + expf(-z)) : expf(z) / (1.f + expf(z));
                     dl = (sig - y) * g.inv_b;
                     if (lane == 0) {
@@ -369,7 +379,7 @@ __global__ void __launch_bounds__(kTW * 32) tail_tc_kernel(TailArgs g) {
 
 template <int AW>
 constexpr size_t tail_smem() {
-    return (size_t)(2 * 64 * kTP + 6 * kTQ * kTP + kTW * 64 + 2 * kTW + kTQ * (AW + 1) * 64) * 4;
+    return (size_t)(2 * 64 * kTP + 6 * kTQ * kTP + kTW * 64 + 2 * kTW + kTQ * (AW + 1) * 64 + kTailLabels) * 4;
 }
 
 using TailKernel = void (*)(TailArgs);
@@ -429,10 +439,18 @@ extern "C" int wj_encoder_tail(const float *pooled, const float *s, const float 
     // inference: one CTA per 16 queries
     const int64_t rows = labels ? partial_rows : (n_batch + kTQ - 1) / kTQ;
     g.per_cta = (int)((n_batch + rows - 1) / rows);
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) {
-        set_error("tail smem attribute: %s", cudaGetErrorString(e));
-        return WJ_ERR_CUDA;
+    // the smem attribute is per (device, kernel): set once (a repeat is harmless)
+    static bool attr_done[64][17] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaError_t e = cudaSuccess;
+    if (dev < 0 || dev >= 64 || !attr_done[dev][aw]) {
+        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) {
+            set_error("tail smem attribute: %s", cudaGetErrorString(e));
+            return WJ_ERR_CUDA;
+        }
+        if (dev >= 0 && dev < 64) attr_done[dev][aw] = true;
     }
     e = launch_pdl(k, dim3((unsigned)rows), dim3(kTW * 32), smem, (cudaStream_t)stream, g);
     if (e != cudaSuccess) {

@@ -363,7 +363,7 @@ class TrainStep:
     def __init__(self, store: SubgraphStore, params: E.ModelParams, state: E.AdamState,
                  dense_dtype=torch.float32, mode: str = "fused", use_graph: bool = True,
                  process_group=None, seed: int = 0, fast_tail: Optional[bool] = None,
-                 features: Optional[torch.Tensor] = None, overlap_inputs: bool = False):
+                 features: Optional[torch.Tensor] = None, overlap_inputs: bool = False, launch: str = "graph"):
         if features is not None and mode == "fused":
             raise ValueError("node features need mode='pooled' or 'reference' (the fused kernel is RPE-only)")
         self.store, self.params, self.state = store, params, state
@@ -399,6 +399,16 @@ class TrainStep:
             self.loss_buf = torch.zeros(1, dtype=torch.float32, device=self.dev)
             if process_group is not None:  # data parallel: [grads | loss] all-reduced
                 self.grad_flat = torch.zeros(int(self.offs[-1]) + 1, dtype=torch.float32, device=self.dev)
+        if launch not in ("graph", "chain"):
+            raise ValueError(f"launch must be 'graph' or 'chain', got {launch!r}")
+        # "chain": the native step executor (wj_stepper_*): three programmatic-
+        # dependent launches per step, consecutive steps chained on the stream
+        self.launch = launch if (self.fast_tail and process_group is None) else "graph"
+        self._stepper = None
+        self._stepper_cap = 0
+        self._loss_hist = None
+        self._n_calls = 0
+        self.input_event = None
 
     def _buffers(self, B, A):
         if self.mode == "fused":
@@ -474,11 +484,90 @@ class TrainStep:
         self._host_bc[1] = 1.0 / (1.0 - self.state.beta2 ** t)
         self.inv_bc.copy_(self._host_bc, non_blocking=True)
 
-    def __call__(self, q: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
+    # ------------------------------------------------------------ chain mode
+    _LOSS_HIST = 4096
+
+    def _make_stepper(self, B: int):
+        from . import _lib
+
+        st, p, store = self.state, self.params, self.store
+        A, W = p.arity, store.width
+        if self._stepper is not None:
+            _lib.load().wj_stepper_destroy(self._stepper)
+            self._stepper = None
+        cap = max(B, 16)
+        rows_max = max(1, min((cap + 15) // 16, self.tail_rows))
+        self._chain_bufs = {"pooled": torch.empty((cap, 64), device=self.dev),
+                            "S": torch.empty((cap, A * W, 64), device=self.dev),
+                            "msum": torch.empty((cap, 64), device=self.dev),
+                            "partial": torch.empty((rows_max, int(self.offs[-1]) + 1), device=self.dev)}
+        b = self._chain_bufs
+        keep = (1.0 - p.dropout) if p.dropout > 0.0 else 1.0
+        h = ctypes.c_void_p()
+        if store.voff_d is None:
+            store.build_vindex()
+        _lib.call("wj_stepper_create", _lib.ptr(store.offsets_d), _lib.ptr(store.uniq_x_d),
+                  _lib.ptr(store.uniq_id_d), *store.vindex_ptrs(),
+                  A, store.num_walks, store.walk_steps, store.max_unique, _lib.ptr(self.flat),
+                  _lib.ptr(self.m_flat), _lib.ptr(self.v_flat), self.offs_c, keep,
+                  1.0 / (keep * A * store.landings), self.seed & ((1 << 64) - 1),
+                  st.lr, st.beta1, st.beta2, st.eps, _lib.ptr(self.step_t), _lib.ptr(b["pooled"]),
+                  _lib.ptr(b["S"]), _lib.ptr(b["msum"]), _lib.ptr(b["partial"]), rows_max, ctypes.byref(h))
+        self._stepper, self._stepper_cap = h, cap
+        if self._loss_hist is None:
+            self._loss_hist = torch.zeros(self._LOSS_HIST, dtype=torch.float32, device=self.dev)
+
+    def _chain_call(self, q: torch.Tensor, y: torch.Tensor, loss_out=None) -> torch.Tensor:
+        from . import _lib
+
+        B = q.shape[0]
+        if q.device.type == "cpu" and not q.is_pinned():
+            q = q.to(self.dev)
+        if y.device.type == "cpu" and not y.is_pinned():
+            y = y.to(self.dev, torch.float32)
+        if y.dtype != torch.float32:
+            y = y.to(torch.float32)
+        q = q.contiguous()
+        if self._stepper is None or B > self._stepper_cap:
+            self._make_stepper(B)
+        i = self._n_calls % self._LOSS_HIST
+        self._n_calls += 1
+        out = self._loss_hist[i] if loss_out is None else loss_out
+        _lib.call("wj_stepper_run", self._stepper, q.data_ptr(), y.data_ptr(), B, out.data_ptr(),
+                  _lib.stream_handle(self.dev))
+        if q.device.type == "cpu" or y.device.type == "cpu":
+            # host inputs are read in place: their buffers are free once this completes
+            if not hasattr(self, "_events"):
+                self._events = [torch.cuda.Event() for _ in range(16)]
+            ev = self._events[i % 16]
+            ev.record()
+            self.input_event = ev
+        else:
+            self.input_event = None
+        self.params.version += 1
+        return out
+
+    def __del__(self):
+        try:
+            if getattr(self, "_stepper", None) is not None:
+                from . import _lib
+
+                _lib.load().wj_stepper_destroy(self._stepper)
+                self._stepper = None
+        except Exception:
+            pass
+
+    def __call__(self, q: torch.Tensor, y: torch.Tensor, loss_out: Optional[torch.Tensor] = None) -> torch.Tensor:
         """q: [B, A] int64 ids, y: [B] labels (device, or pinned host for the
-        end-to-end path).  Returns the loss (device scalar)."""
+        end-to-end path).  Returns the loss (device scalar, valid in stream
+        order).  ``launch="chain"``: the inputs are read by the kernels in
+        place (pinned host memory stays untouched until the step completes)
+        and ``loss_out`` (a one-element device or pinned host tensor)
+        optionally receives the loss instead."""
         B, A = q.shape
         self._prepare_bc()
+        if self.launch == "chain":
+            return self._chain_call(q, y, loss_out)
         if not self.use_graph:
             qd, yd = q.to(self.dev, non_blocking=True), y.to(self.dev, self.params.w1.dtype, non_blocking=True)
             self.input_event = torch.cuda.Event()

@@ -1,7 +1,7 @@
 """Kernel timeline of the C3 training step (torch.profiler / CUPTI): start,
 duration and gap of every kernel / memcpy in a few steady-state steps.
 
-    python profiles/step_timeline.py
+    python profiles/step_timeline.py [graph|chain]
 """
 import os
 import sys
@@ -26,7 +26,8 @@ def main():
     yd = [torch.from_numpy(y).to(dev) for _, y in plan]
     p = wj.init_params(2, cfg["L"], dropout=0.1, seed=11, device=dev)
     st = wj.AdamState.for_params(p)
-    step = wj.TrainStep(store, p, st, use_graph=True, seed=3, overlap_inputs=True)
+    launch = sys.argv[1] if len(sys.argv) > 1 else "graph"
+    step = wj.TrainStep(store, p, st, use_graph=True, seed=3, overlap_inputs=True, launch=launch)
     for k in range(5):
         step(qd[k], yd[k])
     torch.cuda.synchronize()

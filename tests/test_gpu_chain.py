@@ -1,0 +1,84 @@
+"""The native step executor (``TrainStep(launch="chain")``, wj_stepper_*):
+three programmatic-dependent launches per step, consecutive steps chained on
+one stream, inputs read in place (device or pinned host memory).  It must
+give exactly the graph-mode step's results -- same kernels, same dropout
+stream, same fixed-order reductions -- step after step, for varying batch
+sizes, and with the loss written straight into pinned host memory."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def store_and_batches():
+    import paper_2202_13538_b200 as wj
+
+    rng = np.random.default_rng(5)
+    g = wj.Graph.from_edges(rng.integers(0, 3000, size=(30000, 2)), 3000)
+    s = wj.preprocess(g, 50, 4, 9)
+    batches = []
+    for B in (330, 330, 200, 330, 17, 400, 330, 1):
+        q = torch.from_numpy(np.stack([rng.choice(3000, 2, replace=False) for _ in range(B)]).astype(np.int64))
+        y = torch.from_numpy((rng.random(B) < 0.2).astype(np.float32))
+        batches.append((q, y))
+    return s, batches
+
+
+def _run(store, batches, launch, where):
+    import paper_2202_13538_b200 as wj
+
+    p = wj.init_params(2, 4, dropout=0.1, seed=3)
+    st = wj.AdamState.for_params(p, lr=1e-3)
+    step = wj.TrainStep(store, p, st, use_graph=True, seed=77, launch=launch, overlap_inputs=True)
+    assert step.launch == launch
+    losses = []
+    for q, y in batches:
+        if where == "device":
+            q, y = q.cuda(), y.cuda()
+        else:
+            q, y = q.pin_memory(), y.pin_memory()
+        if launch == "chain" and where == "pinned":
+            out = torch.zeros(1, dtype=torch.float32).pin_memory()
+            step(q, y, loss_out=out)
+            torch.cuda.synchronize()
+            losses.append(float(out[0]))
+        else:
+            losses.append(float(step(q, y)))
+    torch.cuda.synchronize()
+    return {k: v.detach().clone() for k, v in p.tensors.items()}, losses, int(step.step_t.item())
+
+
+@pytest.mark.parametrize("where", ["device", "pinned"])
+def test_chain_equals_graph(store_and_batches, where):
+    store, batches = store_and_batches
+    pg, lg, tg = _run(store, batches, "graph", where)
+    pc, lc, tc = _run(store, batches, "chain", where)
+    assert tg == tc == len(batches)
+    assert lg == lc
+    for k in pg:
+        assert torch.equal(pg[k], pc[k]), k
+
+
+def test_chain_back_to_back_without_syncs(store_and_batches):
+    """Many chained steps enqueued with no host sync in between (the PDL
+    chain proper) end in the same parameters as the graph path."""
+    import paper_2202_13538_b200 as wj
+
+    store, batches = store_and_batches
+    seq = [batches[k % 4] for k in range(40)]
+    outs = []
+    for launch in ("graph", "chain"):
+        p = wj.init_params(2, 4, dropout=0.1, seed=3)
+        st = wj.AdamState.for_params(p, lr=1e-3)
+        step = wj.TrainStep(store, p, st, use_graph=True, seed=5, launch=launch, overlap_inputs=True)
+        qd = [(q.cuda(), y.cuda()) for q, y in seq]
+        torch.cuda.synchronize()
+        for q, y in qd:
+            step(q, y)
+        torch.cuda.synchronize()
+        outs.append({k: v.clone() for k, v in p.tensors.items()})
+    for k in outs[0]:
+        assert torch.equal(outs[0][k], outs[1][k]), k
