@@ -232,7 +232,10 @@ int wj_adam(float *params, float *m, float *v, const float *partial, int32_t par
  * (the store's index, flat params / Adam moments at offsets9, work buffers
  * pooled [B_max, 64], s_out [B_max, A*(L+1), 64], msum [B_max, 64],
  * partial [partial_rows_max, n_params + 1], the device step counter,
- * tail_scale = 1 / (keep_prob * A * M * (L+1)) as wj_encoder_tail takes it) fixed
+ * tail_scale = 1 / (keep_prob * A * M * (L+1)) as wj_encoder_tail takes it,
+ * sched: NULL, or two zeroed int32 in device memory owned by this stepper --
+ * the join+encode kernel then grabs queries dynamically from a counter
+ * there and resets it when done) fixed
  * at creation.  All three launches are programmatic-dependent, so
  * consecutive runs on one stream form a single PDL chain: the next step's
  * join+encode kernel stages its first query while this step's tail and Adam
@@ -248,7 +251,7 @@ int wj_stepper_create(const int64_t *offsets, const int32_t *uniq_x, const int32
                       float *adam_v, const int32_t *offsets9, float keep_prob, float tail_scale, uint64_t seed,
                       float lr, float beta1,
                       float beta2, float eps, int64_t *step, float *pooled, float *s_out, float *msum,
-                      float *partial, int32_t partial_rows_max, wj_stepper **out);
+                      float *partial, int32_t partial_rows_max, int32_t *sched, wj_stepper **out);
 int wj_stepper_run(wj_stepper *stepper, const int64_t *queries, const float *labels, int64_t n_batch,
                    float *loss_out, wj_stream_t stream);
 int wj_stepper_destroy(wj_stepper *stepper);

@@ -47,7 +47,7 @@ SIGNATURES = {
                 P, P, P, P],
     "wj_sum_partials": [P, I32, I32, P, P],
     "wj_stepper_create": [P, P, P, P, P, P, P, I32, I32, I32, I32, P, P, P, P, ctypes.c_float, ctypes.c_float, U64,
-                          ctypes.c_float, ctypes.c_float, ctypes.c_float, ctypes.c_float, P, P, P, P, P, I32, P],
+                          ctypes.c_float, ctypes.c_float, ctypes.c_float, ctypes.c_float, P, P, P, P, P, I32, P, P],
     "wj_stepper_run": [P, P, P, I64, P, P],
     "wj_stepper_destroy": [P],
     "wj_gather_rpe": [P, I64, P, I64, I32, P, I32, P, P],

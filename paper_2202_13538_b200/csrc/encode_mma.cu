@@ -53,7 +53,7 @@ struct QMeta {
     int64_t lo, vo;  // first entry of the anchor's sorted list / of its virtual landings
     int u, v2, v1;   // list length, 2-row and 1-row virtual landings
 };
-constexpr int kHdrBytes = (kMetaQ * 3 * (int)sizeof(QMeta) + 16 + 32 + 15) & ~15;  // meta | wscale[4] | wred[8]
+constexpr int kHdrBytes = (kMetaQ * 3 * (int)sizeof(QMeta) + 16 + 32 + 16 + 15) & ~15;  // meta | wscale[4] | wred[8] | next_b
 
 struct EncMmaArgs {
     const int64_t *queries;
@@ -75,6 +75,7 @@ struct EncMmaArgs {
     float *pooled;  // [B, 64]
     float *s_out;   // [B, AW, 64] or null
     float *msum;    // [B, 64] or null
+    int32_t *qsched;  // [2] zeroed query-grab / done counters (dynamic scheduling) or null: static striding
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -332,7 +333,32 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
             meta[t] = m;
         }
     };
-    load_meta(blockIdx.x);
+    // Query scheduling.  Static: CTA c takes queries c, c + grid, ...
+    // (metadata kMetaQ at a time).  Dynamic (g.qsched): the first query is
+    // blockIdx.x, every further one is grabbed from a global counter once the
+    // previous one's tiles start, its metadata loaded while that query's
+    // reduction runs -- CTAs that run ahead (or start early under PDL) take
+    // more queries.  The last CTA to finish resets the counters.
+    const bool dyn = g.qsched != nullptr;
+    int64_t *next_b = reinterpret_cast<int64_t *>(wscale + 12);
+    auto load_meta1 = [&](int64_t bb, QMeta *dst) {
+        if (threadIdx.x < A) {
+            QMeta m = {0, 0, 0, 0, 0};
+            if (bb < g.n_batch) {
+                const int64_t q = g.queries[bb * A + threadIdx.x];
+                m.lo = g.offsets[q];
+                m.u = (int)(g.offsets[q + 1] - m.lo);
+                m.vo = g.voff[q];
+                m.v2 = g.vcnt[2 * q];
+                m.v1 = g.vcnt[2 * q + 1];
+            }
+            dst[threadIdx.x] = m;
+        }
+    };
+    if (dyn)
+        load_meta1(blockIdx.x, meta);
+    else
+        load_meta(blockIdx.x);
     __syncthreads();
     float *wred = wscale + 4;  // [kMW] W^T max-reduction scratch (the rows area is live by then)
 
@@ -370,13 +396,13 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
     uint64_t skey = 0;
 
     int jq = 0;  // local query index
-    for (int64_t b = blockIdx.x; b < g.n_batch; b += gridDim.x, ++jq) {
-        if (jq > 0 && jq % kMetaQ == 0) {  // metadata of the CTA's next kMetaQ queries
+    for (int64_t b = blockIdx.x; b < g.n_batch; ++jq) {
+        if (!dyn && jq > 0 && jq % kMetaQ == 0) {  // metadata of the CTA's next kMetaQ queries
             __syncthreads();
             load_meta(b);
             __syncthreads();
         }
-        const QMeta *qm = meta + (jq % kMetaQ) * A;
+        const QMeta *qm = dyn ? meta + (jq & 1) * A : meta + (jq % kMetaQ) * A;
         int U[A], V2[A], V1[A], pu[A + 1], p2[A + 1], p1[A + 1];
         pu[0] = p2[0] = p1[0] = 0;
 #pragma unroll
@@ -434,7 +460,8 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
             stage_wt();
         }
         // last query of this CTA, after the wait: dependents may launch
-        if (b + gridDim.x >= g.n_batch) pdl_trigger();
+        if (!dyn && b + gridDim.x >= g.n_batch) pdl_trigger();
+        if (dyn && threadIdx.x == 0) *next_b = (int64_t)gridDim.x + atomicAdd(g.qsched, 1);
 
         // ---- per-warp tiles of 16 virtual landings
         uint32_t qq = (uint32_t)mix64(skey ^ mix64((uint64_t)b));
@@ -457,6 +484,12 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
                 tile<false>(vl + v0, xr_s, wt_s, lane, cq, g.t11, 0u, sacc);
         }
         __syncthreads();  // rows are dead: red overlays them
+        int64_t nb = b + gridDim.x;
+        if (dyn) {
+            nb = *next_b;
+            if (nb >= g.n_batch) pdl_trigger();
+            load_meta1(nb, meta + ((jq + 1) & 1) * A);  // lands while the reduction runs
+        }
         // ---- CTA reduction: per-warp S^T partials -> smem -> fixed-order sum
         float *myred = red + warp * H * kRedS;
 #pragma unroll
@@ -494,6 +527,14 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
             g.pooled[b * H + m] = s;
         }
         __syncthreads();
+        b = nb;
+    }
+    if (dyn && threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(g.qsched + 1, 1) == (int)gridDim.x - 1) {  // every CTA is done grabbing
+            atomicExch(g.qsched, 0);
+            atomicExch(g.qsched + 1, 0);
+        }
     }
 }
 
@@ -766,7 +807,7 @@ extern "C" int wj_stepper_create(const int64_t *offsets, const int32_t *uniq_x, 
                                  int32_t max_unique, float *params, float *adam_m, float *adam_v,
                                  const int32_t *offsets9, float keep_prob, float tail_scale, uint64_t seed, float lr, float beta1,
                                  float beta2, float eps, int64_t *step, float *pooled, float *s_out, float *msum,
-                                 float *partial, int32_t partial_rows_max, wj_stepper **out) {
+                                 float *partial, int32_t partial_rows_max, int32_t *sched, wj_stepper **out) {
     using namespace wj;
     if (!out || !params || !adam_m || !adam_v || !offsets9 || !step || !pooled || !s_out || !msum || !partial ||
         partial_rows_max < 1 || arity < 1 || num_walks < 1 || num_steps < 1 || !(keep_prob > 0.f) || keep_prob > 1.f) {
@@ -796,6 +837,7 @@ extern "C" int wj_stepper_create(const int64_t *offsets, const int32_t *uniq_x, 
     st->args.pooled = pooled;
     st->args.s_out = s_out;
     st->args.msum = msum;
+    st->args.qsched = sched;
     st->arity = arity;
     st->aw = arity * (num_steps + 1);
     st->tail_rows_max = partial_rows_max;

@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import ctypes
 import logging
+import os
 import time
 from collections import deque
 from dataclasses import dataclass, field
@@ -406,6 +407,9 @@ class TrainStep:
         self.launch = launch if (self.fast_tail and process_group is None) else "graph"
         self._stepper = None
         self._stepper_cap = 0
+        # chain mode: the join+encode kernel grabs queries from a device counter
+        self.dynamic_queries = os.environ.get("WJ_DYNAMIC_QUERIES", "1") != "0"
+        self._sched = torch.zeros(2, dtype=torch.int32, device=self.dev)
         self._loss_hist = None
         self._n_calls = 0
         self.input_event = None
@@ -512,7 +516,8 @@ class TrainStep:
                   _lib.ptr(self.m_flat), _lib.ptr(self.v_flat), self.offs_c, keep,
                   1.0 / (keep * A * store.landings), self.seed & ((1 << 64) - 1),
                   st.lr, st.beta1, st.beta2, st.eps, _lib.ptr(self.step_t), _lib.ptr(b["pooled"]),
-                  _lib.ptr(b["S"]), _lib.ptr(b["msum"]), _lib.ptr(b["partial"]), rows_max, ctypes.byref(h))
+                  _lib.ptr(b["S"]), _lib.ptr(b["msum"]), _lib.ptr(b["partial"]), rows_max,
+                  _lib.ptr(self._sched) if self.dynamic_queries else None, ctypes.byref(h))
         self._stepper, self._stepper_cap = h, cap
         if self._loss_hist is None:
             self._loss_hist = torch.zeros(self._LOSS_HIST, dtype=torch.float32, device=self.dev)
@@ -739,7 +744,8 @@ def train(store: SubgraphStore, split, cfg: TrainConfig, features=None, train_ne
     pool = _rows(train_negatives) if train_negatives is not None and len(train_negatives) else None
     feats_d = None if features is None else torch.as_tensor(features, dtype=torch.float32, device=dev)
     step = TrainStep(store, params, state, mode="fused" if feats_d is None else "pooled",
-                     use_graph=use_graph, seed=derive_seed(cfg.seed, "dropout"), features=feats_d)
+                     use_graph=use_graph, seed=derive_seed(cfg.seed, "dropout"), features=feats_d,
+                     launch="chain" if use_graph else "graph")
     planner = None
     if native_planner and arity <= 4:
         planner = BatchPlanner(positives, np.concatenate(filt_rows), store.num_nodes, cfg, batch_rng, pool=pool)
@@ -750,10 +756,20 @@ def train(store: SubgraphStore, split, cfg: TrainConfig, features=None, train_ne
         consumed, n_steps = 0, 0
         loss_sum = torch.zeros((), dtype=torch.float64, device=dev)
         if planner is not None:  # native planner, producer thread ahead of the device
+            pending = []  # chain mode: per-step loss slots, summed in blocks (keeps the PDL chain intact)
             for q, y, _ in planner.epoch():
-                loss_sum += step(q, y).double()
+                loss = step(q, y)
+                if step.launch == "chain":
+                    pending.append(loss)
+                    if len(pending) == TrainStep._LOSS_HIST // 2:
+                        loss_sum += torch.stack(pending).double().sum()
+                        pending = []
+                else:
+                    loss_sum += loss.double()
                 planner.release(step.input_event)
                 n_steps += 1
+            if pending:
+                loss_sum += torch.stack(pending).double().sum()
         while planner is None and consumed < positives.shape[0]:
             seeds, ids = sample_minibatch(index, positives, cfg, batch_rng, exact=exact_batches)
             if not ids:

@@ -62,7 +62,8 @@ def test_chain_equals_graph(store_and_batches, where):
         assert torch.equal(pg[k], pc[k]), k
 
 
-def test_chain_back_to_back_without_syncs(store_and_batches):
+@pytest.mark.parametrize("dynamic", [True, False])
+def test_chain_back_to_back_without_syncs(store_and_batches, dynamic):
     """Many chained steps enqueued with no host sync in between (the PDL
     chain proper) end in the same parameters as the graph path."""
     import paper_2202_13538_b200 as wj
@@ -74,6 +75,7 @@ def test_chain_back_to_back_without_syncs(store_and_batches):
         p = wj.init_params(2, 4, dropout=0.1, seed=3)
         st = wj.AdamState.for_params(p, lr=1e-3)
         step = wj.TrainStep(store, p, st, use_graph=True, seed=5, launch=launch, overlap_inputs=True)
+        step.dynamic_queries = dynamic  # join+encode grabs queries from a counter (chain mode)
         qd = [(q.cuda(), y.cuda()) for q, y in seq]
         torch.cuda.synchronize()
         for q, y in qd:
