@@ -23,6 +23,8 @@ import logging
 from dataclasses import dataclass
 from typing import Iterable, Optional, Sequence
 
+import warnings
+
 import numpy as np
 import torch
 
@@ -189,11 +191,15 @@ class DeviceGraph:
         if n >= 2 ** 31:
             raise ValueError("graphs with >= 2^31 nodes are not supported")
         idxptr = np.asarray(g.idxptr)
-        indices = np.ascontiguousarray(np.asarray(g.indices), dtype=np.int32)
         small = idxptr.shape[0] == 0 or int(idxptr[-1]) < 2 ** 31
-        ip = torch.from_numpy(np.array(idxptr, dtype=np.int32 if small else np.int64))
-        return cls(n, ip.to(device), torch.from_numpy(np.array(indices, dtype=np.int32)).to(device),
-                   getattr(g, "id_map", None))
+        ip = np.ascontiguousarray(idxptr, dtype=np.int32 if small else np.int64)
+        # no host-side copy of the (large) indices array when it is already
+        # contiguous int32; read-only arrays are fine for the H2D copy
+        ix = np.ascontiguousarray(np.asarray(g.indices), dtype=np.int32)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", UserWarning)  # non-writable numpy view: torch only reads it
+            ipt, ixt = torch.from_numpy(ip), torch.from_numpy(ix)
+        return cls(n, ipt.to(device), ixt.to(device), getattr(g, "id_map", None))
 
     def to_host(self) -> Graph:
         return Graph(self.num_nodes, self.idxptr.cpu().numpy().astype(np.int64),

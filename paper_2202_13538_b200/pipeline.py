@@ -346,6 +346,73 @@ class BatchPlanner:
             pass
 
 
+class DeviceFeeder:
+    """Planner batches (pinned host slots) -> a device ring, for the chain
+    executor: each batch's H2D copy is issued on a side stream one batch
+    ahead and its completion is checked on the HOST before the batch is
+    handed out, so the training stream carries no copy or wait between steps
+    and its programmatic-dependent chain stays unbroken (the kernels then
+    read device memory, not mapped host memory: ~5 us per step less at C3).
+    A device slot is overwritten only after the step that read it (the
+    consumer calls ``consumed()`` after each step)."""
+
+    def __init__(self, planner: "BatchPlanner", device, depth: int = 4):
+        self.planner, self.dev, self.depth = planner, torch.device(device), int(depth)
+        self.q = torch.empty((self.depth, planner.cap, planner.arity), dtype=torch.int64, device=self.dev)
+        self._ycache = {}
+        self.stream = torch.cuda.Stream(self.dev)
+        self.copied = [torch.cuda.Event() for _ in range(self.depth)]
+        self.done = [torch.cuda.Event() for _ in range(self.depth)]
+        self._used = [False] * self.depth
+        self._cur = None
+        self._k = 0
+
+    def _labels(self, B: int, n_pos: int) -> torch.Tensor:
+        # the planner's labels are 1 for the first n_pos queries, 0 after:
+        # one resident device vector per (B, n_pos) instead of a copy per step
+        y = self._ycache.get((B, n_pos))
+        if y is None:
+            y = torch.zeros(B, dtype=torch.float32, device=self.dev)
+            y[:n_pos] = 1.0
+            self._ycache[(B, n_pos)] = y
+        return y
+
+    def _issue(self, batch):
+        q, y, n_pos = batch
+        s = self._k % self.depth
+        self._k += 1
+        B = int(q.shape[0])
+        if self._used[s]:  # the step that last read this slot
+            self.stream.wait_event(self.done[s])
+        with torch.cuda.stream(self.stream):
+            self.q[s, :B].copy_(q, non_blocking=True)
+            self.copied[s].record(self.stream)
+        self.planner.release(self.copied[s])  # the pinned slot is free once copied
+        return s, B, n_pos
+
+    def epoch(self):
+        """Yields (q, y, n_pos) device views, one epoch of the planner."""
+        it = self.planner.epoch()
+        try:
+            b = next(it, None)
+            nxt = self._issue(b) if b is not None else None
+            while nxt is not None:
+                s, B, n_pos = nxt
+                b = next(it, None)
+                nxt = self._issue(b) if b is not None else None
+                self.copied[s].synchronize()  # long complete: issued a step ago
+                self._cur = s
+                yield self.q[s, :B], self._labels(B, n_pos), n_pos
+        finally:
+            it.close()
+
+    def consumed(self) -> None:
+        """Call after enqueueing the step that reads the last batch."""
+        s = self._cur
+        self.done[s].record(torch.cuda.current_stream(self.dev))
+        self._used[s] = True
+
+
 class TrainStep:
     """One training step on the device, captured as CUDA graphs per batch
     shape (``use_graph``; two graphs with their own input buffers, so the
@@ -410,6 +477,7 @@ class TrainStep:
         # chain mode: the join+encode kernel grabs queries from a device counter
         self.dynamic_queries = os.environ.get("WJ_DYNAMIC_QUERIES", "1") != "0"
         self._sched = torch.zeros(2, dtype=torch.int32, device=self.dev)
+        self.record_input_events = True
         self._loss_hist = None
         self._n_calls = 0
         self.input_event = None
@@ -540,7 +608,7 @@ class TrainStep:
         out = self._loss_hist[i] if loss_out is None else loss_out
         _lib.call("wj_stepper_run", self._stepper, q.data_ptr(), y.data_ptr(), B, out.data_ptr(),
                   _lib.stream_handle(self.dev))
-        if q.device.type == "cpu" or y.device.type == "cpu":
+        if (q.device.type == "cpu" or y.device.type == "cpu") and self.record_input_events:
             # host inputs are read in place: their buffers are free once this completes
             if not hasattr(self, "_events"):
                 self._events = [torch.cuda.Event() for _ in range(16)]
@@ -746,30 +814,34 @@ def train(store: SubgraphStore, split, cfg: TrainConfig, features=None, train_ne
     step = TrainStep(store, params, state, mode="fused" if feats_d is None else "pooled",
                      use_graph=use_graph, seed=derive_seed(cfg.seed, "dropout"), features=feats_d,
                      launch="chain" if use_graph else "graph")
-    planner = None
+    planner = feeder = None
     if native_planner and arity <= 4:
         planner = BatchPlanner(positives, np.concatenate(filt_rows), store.num_nodes, cfg, batch_rng, pool=pool)
+        feeder = DeviceFeeder(planner, dev)
     history = []
     best_params, best_metric, best_epoch = params.copy(), -np.inf, 0
     for epoch in range(1, cfg.max_epochs + 1):
         t0 = time.perf_counter()
         consumed, n_steps = 0, 0
         loss_sum = torch.zeros((), dtype=torch.float64, device=dev)
-        if planner is not None:  # native planner, producer thread ahead of the device
-            pending = []  # chain mode: per-step loss slots, summed in blocks (keeps the PDL chain intact)
-            for q, y, _ in planner.epoch():
-                loss = step(q, y)
-                if step.launch == "chain":
-                    pending.append(loss)
-                    if len(pending) == TrainStep._LOSS_HIST // 2:
-                        loss_sum += torch.stack(pending).double().sum()
-                        pending = []
-                else:
-                    loss_sum += loss.double()
-                planner.release(step.input_event)
+        if planner is not None and step.launch == "chain":
+            # native planner -> device ring -> chain executor; per-step losses
+            # stay in the executor's ring and are summed in blocks
+            pending = []
+            for q, y, _ in feeder.epoch():
+                pending.append(step(q, y))
+                feeder.consumed()
                 n_steps += 1
+                if len(pending) == TrainStep._LOSS_HIST // 2:
+                    loss_sum += torch.stack(pending).double().sum()
+                    pending = []
             if pending:
                 loss_sum += torch.stack(pending).double().sum()
+        elif planner is not None:  # native planner, graph steps on pinned batches
+            for q, y, _ in planner.epoch():
+                loss_sum += step(q, y).double()
+                planner.release(step.input_event)
+                n_steps += 1
         while planner is None and consumed < positives.shape[0]:
             seeds, ids = sample_minibatch(index, positives, cfg, batch_rng, exact=exact_batches)
             if not ids:
