@@ -169,6 +169,48 @@ __global__ void __launch_bounds__(kRpeWarps * 32) rpe_kernel(
     }
 }
 
+// Count-only pass: the number of distinct landings of each anchor, which
+// only sizes the fill pass, needs no sort -- each warp inserts its anchor's
+// P landings into an open-addressing set in shared memory (atomicCAS, load
+// <= 1/2) and counts the successful inserts.  Same result as the sort's
+// segment-head count.
+constexpr int kCountWarps = 8;
+
+__global__ void __launch_bounds__(kCountWarps * 32) rpe_count_hash_kernel(
+    const int32_t *__restrict__ walks, int64_t n_anchors, int P, int tbits, int32_t *__restrict__ counts_out) {
+    extern __shared__ __align__(16) uint32_t tabs[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int T = 1 << tbits;
+    uint32_t *tab = tabs + (size_t)warp * T;
+    for (int64_t k = (int64_t)blockIdx.x * kCountWarps + warp; k < n_anchors;
+         k += (int64_t)gridDim.x * kCountWarps) {
+        for (int i = lane * 4; i < T; i += 128) *reinterpret_cast<uint4 *>(tab + i) = make_uint4(~0u, ~0u, ~0u, ~0u);
+        __syncwarp();
+        const int32_t *src = walks + k * (int64_t)P;
+        int count = 0;
+        for (int base = 0; base < P; base += 32) {
+            const int i = base + lane;
+            bool fresh = false;
+            if (i < P) {
+                const uint32_t x = (uint32_t)__ldg(src + i);
+                uint32_t h = (x * 0x9E3779B1u) >> (32 - tbits);
+                while (true) {
+                    const uint32_t old = atomicCAS(tab + h, ~0u, x);
+                    if (old == ~0u) {
+                        fresh = true;
+                        break;
+                    }
+                    if (old == x) break;
+                    h = (h + 1) & (T - 1);
+                }
+            }
+            count += __popc(__ballot_sync(kFull, fresh));
+        }
+        if (lane == 0) counts_out[k] = count;
+        __syncwarp();
+    }
+}
+
 static int make_shape(int32_t M, int32_t L, int64_t n_nodes, RpeShape &sh, bool &wide) {
     if (M < 1 || L < 1) {
         set_error("num_walks and num_steps must be >= 1");
@@ -230,6 +272,25 @@ extern "C" int wj_rpe_count(const int32_t *walks, int64_t n_anchors, int32_t num
     int rc = make_shape(num_walks, num_steps, n_nodes, sh, wide);
     if (rc) return rc;
     cudaStream_t s = (cudaStream_t)stream;
+    if (sh.P <= 2048) {  // hash-set count (table <= 16 KB per warp)
+        if (n_anchors == 0) return WJ_OK;
+        const int tbits = bits_for((uint64_t)(2 * sh.P - 1)) < 5 ? 5 : bits_for((uint64_t)(2 * sh.P - 1));
+        const size_t smem = ((size_t)1 << tbits) * 4 * kCountWarps;
+        cudaError_t e = cudaFuncSetAttribute(rpe_count_hash_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) {
+            set_error("rpe count smem attribute: %s", cudaGetErrorString(e));
+            return WJ_ERR_CUDA;
+        }
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rpe_count_hash_kernel, kCountWarps * 32, smem);
+        int64_t blocks = (n_anchors + kCountWarps - 1) / kCountWarps;
+        const int64_t cap = (int64_t)sm_count() * (per_sm > 0 ? per_sm : 1) * 16;
+        if (blocks > cap) blocks = cap;
+        rpe_count_hash_kernel<<<(unsigned)blocks, kCountWarps * 32, smem, s>>>(walks, n_anchors, sh.P, tbits,
+                                                                               counts_out);
+        return check_launch("wj_rpe_count");
+    }
     if (wide)
         return launch_rpe<uint64_t, false>(walks, n_anchors, sh, counts_out, nullptr, nullptr,
                                            nullptr, nullptr, nullptr, s);
