@@ -458,6 +458,10 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
             pdl_wait();
             skey = mix64(g.seed + kGolden * ((uint64_t)(g.step ? *g.step : 0) + 1ULL));
             stage_wt();
+            // dynamic scheduling: a CTA exits only once the queue is empty, so the
+            // dependent tail kernel may launch now -- its CTAs take the SM slots of
+            // retiring CTAs and stage W2 / U1 / V before they wait for this kernel
+            if (dyn) pdl_trigger();
         }
         // last query of this CTA, after the wait: dependents may launch
         if (!dyn && b + gridDim.x >= g.n_batch) pdl_trigger();
@@ -487,7 +491,6 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
         int64_t nb = b + gridDim.x;
         if (dyn) {
             nb = *next_b;
-            if (nb >= g.n_batch) pdl_trigger();
             load_meta1(nb, meta + ((jq + 1) & 1) * A);  // lands while the reduction runs
         }
         // ---- CTA reduction: per-warp S^T partials -> smem -> fixed-order sum

@@ -183,6 +183,41 @@ __device__ __forceinline__ void warp_mma3(float (&acc)[NT][4], int lane, LA la, 
         for (int r = 0; r < 4; ++r) acc[nt][r] += acc2[nt][r];
 }
 
+// Two products sharing the A operand: acc1 += A B1, acc2 += A B2 (16 x 8
+// each, K = 8 * KS), 3-pass TF32 like warp_mma3; the two chains interleave.
+template <int KS, class LA, class LB1, class LB2>
+__device__ __forceinline__ void warp_mma3_dual(float (&acc1)[4], float (&acc2)[4], int lane, LA la, LB1 lb1,
+                                               LB2 lb2) {
+    const int gq = lane >> 2, tq = lane & 3;
+    float x1[4] = {0.f, 0.f, 0.f, 0.f}, x2[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+        uint32_t ah[4], al[4];
+        tf32_split(la(gq, 8 * ks + tq), ah[0], al[0]);
+        tf32_split(la(gq + 8, 8 * ks + tq), ah[1], al[1]);
+        tf32_split(la(gq, 8 * ks + tq + 4), ah[2], al[2]);
+        tf32_split(la(gq + 8, 8 * ks + tq + 4), ah[3], al[3]);
+        uint32_t bh0, bl0, bh1, bl1, ch0, cl0, ch1, cl1;
+        tf32_split(lb1(8 * ks + tq, gq), bh0, bl0);
+        tf32_split(lb1(8 * ks + tq + 4, gq), bh1, bl1);
+        tf32_split(lb2(8 * ks + tq, gq), ch0, cl0);
+        tf32_split(lb2(8 * ks + tq + 4, gq), ch1, cl1);
+        float(&d1)[4] = (ks & 1) ? x1 : acc1;
+        float(&d2)[4] = (ks & 1) ? x2 : acc2;
+        mma_tf32(d1, al, bh0, bh1);
+        mma_tf32(d2, al, ch0, ch1);
+        mma_tf32(d1, ah, bl0, bl1);
+        mma_tf32(d2, ah, cl0, cl1);
+        mma_tf32(d1, ah, bh0, bh1);
+        mma_tf32(d2, ah, ch0, ch1);
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        acc1[r] += x1[r];
+        acc2[r] += x2[r];
+    }
+}
+
 constexpr int kTW = 8;  // warps per tail CTA
 constexpr int kTailLabels = 64;  // labels per CTA prefetched into shared memory
 
@@ -209,8 +244,40 @@ __global__ void __launch_bounds__(kTW * 32) tail_tc_kernel(TailArgs g) {
     // this CTA's labels (inputs, possibly in mapped host memory): fetched
     // before the wait so their latency overlaps the join+encode kernel
     float *LB = SS + kTQ * (AW + 1) * 64;  // [kTailLabels]
+    float *VS = LB + kTailLabels;           // [64][kTP] V = W2 U1
+    float *C1P = VS + 64 * kTP;             // [64] c1' = b2 U1 + c1
     if (train)
         for (int64_t i = tid; i < min((int64_t)kTailLabels, q_hi - q_lo); i += NT) LB[i] = g.labels[q_lo + i];
+    // V = W2 U1 and c1' = b2 U1 + c1 (parameters only, so before the wait):
+    // z2 = scale pooled V + c1' and g = scale dz2 V^T take one product each
+    // on the critical path instead of two (hq and dhq, needed only for
+    // dU1 / dW2, ride along in the same passes)
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    {
+        const int vm = warp & 3, vn = (warp >> 2) * 32;
+        float va[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) va[i][r] = 0.f;
+        warp_mma3<4, 8>(va, lane, [&](int m, int k) { return W2s[(16 * vm + m) * kTP + k]; },
+                        [&](int k, int n) { return U1s[k * kTP + vn + n]; });
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int r0 = 16 * vm + gq, c = vn + 8 * j + 2 * tq;
+            VS[r0 * kTP + c] = va[j][0];
+            VS[r0 * kTP + c + 1] = va[j][1];
+            VS[(r0 + 8) * kTP + c] = va[j][2];
+            VS[(r0 + 8) * kTP + c + 1] = va[j][3];
+        }
+        if (tid < 64) {
+            float c1p = P[g.off.c1 + tid];
+            for (int k = 0; k < 64; ++k) c1p = fmaf(P[g.off.b2 + k], U1s[k * kTP + tid], c1p);
+            C1P[tid] = c1p;
+        }
+    }
     pdl_wait();     // pooled / S / msum of the join+encode kernel
     pdl_trigger();  // the Adam kernel may get scheduled
     constexpr int NW1 = ((AW + 1) * 64 + NT - 1) / NT;
@@ -246,20 +313,23 @@ __global__ void __launch_bounds__(kTW * 32) tail_tc_kernel(TailArgs g) {
         // wait for W2 / U1 (first chunk) and the pooled rows; S may still be in flight
         if (train) cp_async_wait_group1(); else cp_async_wait_all();
         __syncthreads();
-        // hq = scale * pooled W2 + b2 ; z2 = hq U1 + c1   (warp w: output columns 8w .. 8w+7)
-#pragma unroll
-        for (int pass = 0; pass < 2; ++pass) {
-            const float *X = pass ? HQ : PM, *M = pass ? U1s : W2s, *bias = P + (pass ? g.off.c1 : g.off.b2);
-            const float mul = pass ? 1.f : g.scale;
-            float *Y = pass ? Z2 : HQ;
-            float acc[1][4] = {{0.f, 0.f, 0.f, 0.f}};
-            warp_mma3<1, 8>(acc, lane, [&](int m, int k) { return X[m * kTP + k]; },
-                            [&](int k, int n) { return M[k * kTP + 8 * warp + n]; });
+        // hq = scale pooled W2 + b2 and z2 = scale pooled V + c1' in one pass
+        // (warp w: output columns 8w .. 8w+7)
+        {
+            float ah[4] = {0.f, 0.f, 0.f, 0.f}, az[4] = {0.f, 0.f, 0.f, 0.f};
+            warp_mma3_dual<8>(ah, az, lane, [&](int m, int k) { return PM[m * kTP + k]; },
+                              [&](int k, int n) { return W2s[k * kTP + 8 * warp + n]; },
+                              [&](int k, int n) { return VS[k * kTP + 8 * warp + n]; });
             const int c = 8 * warp + 2 * tq;
-            Y[gq * kTP + c] = fmaf(acc[0][0], mul, bias[c]);
-            Y[gq * kTP + c + 1] = fmaf(acc[0][1], mul, bias[c + 1]);
-            Y[(gq + 8) * kTP + c] = fmaf(acc[0][2], mul, bias[c]);
-            Y[(gq + 8) * kTP + c + 1] = fmaf(acc[0][3], mul, bias[c + 1]);
+            const float *b2 = P + g.off.b2;
+            HQ[gq * kTP + c] = fmaf(ah[0], g.scale, b2[c]);
+            HQ[gq * kTP + c + 1] = fmaf(ah[1], g.scale, b2[c + 1]);
+            HQ[(gq + 8) * kTP + c] = fmaf(ah[2], g.scale, b2[c]);
+            HQ[(gq + 8) * kTP + c + 1] = fmaf(ah[3], g.scale, b2[c + 1]);
+            Z2[gq * kTP + c] = fmaf(az[0], g.scale, C1P[c]);
+            Z2[gq * kTP + c + 1] = fmaf(az[1], g.scale, C1P[c + 1]);
+            Z2[(gq + 8) * kTP + c] = fmaf(az[2], g.scale, C1P[c]);
+            Z2[(gq + 8) * kTP + c + 1] = fmaf(az[3], g.scale, C1P[c + 1]);
             __syncthreads();
         }
         // logits, BCE and dz2 (warp w: queries w, w + 8)
@@ -290,20 +360,22 @@ __global__ void __launch_bounds__(kTW * 32) tail_tc_kernel(TailArgs g) {
         }
         __syncthreads();
         if (!train) continue;
-        // dhq[q][k] = sum_h dz2[q][h] U1[k][h] ; g[q][k] = scale sum_h dhq[q][h] W2[k][h]
-#pragma unroll
-        for (int pass = 0; pass < 2; ++pass) {
-            const float *X = pass ? DHQ : DZ2, *M = pass ? W2s : U1s;
-            float *Y = pass ? G : DHQ;
-            const float mul = pass ? g.scale : 1.f;
-            float acc[1][4] = {{0.f, 0.f, 0.f, 0.f}};
-            warp_mma3<1, 8>(acc, lane, [&](int m, int k) { return X[m * kTP + k]; },
-                            [&](int k, int n) { return M[(8 * warp + n) * kTP + k]; });
+        // dhq[q][k] = sum_h dz2[q][h] U1[k][h] and g[q][k] = scale sum_h dz2[q][h] V[k][h]
+        // (= scale sum_h dhq[q][h] W2[k][h]) in one pass
+        {
+            float ad[4] = {0.f, 0.f, 0.f, 0.f}, ag[4] = {0.f, 0.f, 0.f, 0.f};
+            warp_mma3_dual<8>(ad, ag, lane, [&](int m, int k) { return DZ2[m * kTP + k]; },
+                              [&](int k, int n) { return U1s[(8 * warp + n) * kTP + k]; },
+                              [&](int k, int n) { return VS[(8 * warp + n) * kTP + k]; });
             const int c = 8 * warp + 2 * tq;
-            Y[gq * kTP + c] = acc[0][0] * mul;
-            Y[gq * kTP + c + 1] = acc[0][1] * mul;
-            Y[(gq + 8) * kTP + c] = acc[0][2] * mul;
-            Y[(gq + 8) * kTP + c + 1] = acc[0][3] * mul;
+            DHQ[gq * kTP + c] = ad[0];
+            DHQ[gq * kTP + c + 1] = ad[1];
+            DHQ[(gq + 8) * kTP + c] = ad[2];
+            DHQ[(gq + 8) * kTP + c + 1] = ad[3];
+            G[gq * kTP + c] = ag[0] * g.scale;
+            G[gq * kTP + c + 1] = ag[1] * g.scale;
+            G[(gq + 8) * kTP + c] = ag[2] * g.scale;
+            G[(gq + 8) * kTP + c + 1] = ag[3] * g.scale;
             __syncthreads();
         }
         // dW2 += pooled^T dhq (scaled at the end), dU1 += hq^T dz2
@@ -331,29 +403,31 @@ __global__ void __launch_bounds__(kTW * 32) tail_tc_kernel(TailArgs g) {
     }
     if (g.step_inc && blockIdx.x == 0 && tid == 0) *g.step_inc += 1;
     if (!train) return;
-    // ---- partial row of this CTA: [grads | loss]
+    // ---- partial row of this CTA: [grads | loss], assembled in shared memory
+    // (the W2 / U1 / chunk buffers are dead now) and written coalesced
     float *row = g.partial + (int64_t)blockIdx.x * (g.off.total + 1);
+    float *stage = tsm;  // [total + 1] <= 2 * 64 * kTP + 6 * kTQ * kTP floats, ends before vsm
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         const int r0 = 16 * fm + gq, c = 8 * (fn + j) + 2 * tq;
-        row[g.off.w2 + r0 * 64 + c] = aw2[j][0] * g.scale;
-        row[g.off.w2 + r0 * 64 + c + 1] = aw2[j][1] * g.scale;
-        row[g.off.w2 + (r0 + 8) * 64 + c] = aw2[j][2] * g.scale;
-        row[g.off.w2 + (r0 + 8) * 64 + c + 1] = aw2[j][3] * g.scale;
-        row[g.off.u1 + r0 * 64 + c] = au1[j][0];
-        row[g.off.u1 + r0 * 64 + c + 1] = au1[j][1];
-        row[g.off.u1 + (r0 + 8) * 64 + c] = au1[j][2];
-        row[g.off.u1 + (r0 + 8) * 64 + c + 1] = au1[j][3];
+        stage[g.off.w2 + r0 * 64 + c] = aw2[j][0] * g.scale;
+        stage[g.off.w2 + r0 * 64 + c + 1] = aw2[j][1] * g.scale;
+        stage[g.off.w2 + (r0 + 8) * 64 + c] = aw2[j][2] * g.scale;
+        stage[g.off.w2 + (r0 + 8) * 64 + c + 1] = aw2[j][3] * g.scale;
+        stage[g.off.u1 + r0 * 64 + c] = au1[j][0];
+        stage[g.off.u1 + r0 * 64 + c + 1] = au1[j][1];
+        stage[g.off.u1 + (r0 + 8) * 64 + c] = au1[j][2];
+        stage[g.off.u1 + (r0 + 8) * 64 + c + 1] = au1[j][3];
     }
 #pragma unroll
     for (int i = 0; i < NW1; ++i) {
         const int e = tid + NT * i;
         if (e < AW * 64)
-            row[g.off.w1 + e] = aw1[i];
+            stage[g.off.w1 + e] = aw1[i];
         else if (e < (AW + 1) * 64)
-            row[g.off.b1 + e - AW * 64] = aw1[i];
+            stage[g.off.b1 + e - AW * 64] = aw1[i];
     }
-    if (tid < 128) row[(tid < 64 ? g.off.b2 : g.off.c1) + (tid & 63)] = vacc;
+    if (tid < 128) stage[(tid < 64 ? g.off.b2 : g.off.c1) + (tid & 63)] = vacc;
     vsm[warp * 64 + lane] = du2a;
     vsm[warp * 64 + lane + 32] = du2b;
     if (lane == 0) {
@@ -365,21 +439,24 @@ __global__ void __launch_bounds__(kTW * 32) tail_tc_kernel(TailArgs g) {
         float v = 0.f;
 #pragma unroll
         for (int w = 0; w < kTW; ++w) v += vsm[w * 64 + tid];
-        row[g.off.u2 + tid] = v;
+        stage[g.off.u2 + tid] = v;
     } else if (tid == 64 || tid == 65) {
         float v = 0.f;
 #pragma unroll
         for (int w = 0; w < kTW; ++w) v += vsm[kTW * 64 + (tid - 64) * kTW + w];
         if (tid == 64)
-            row[g.off.c2] = v;
+            stage[g.off.c2] = v;
         else
-            row[g.off.total] = v * g.inv_b;
+            stage[g.off.total] = v * g.inv_b;
     }
+    __syncthreads();
+    for (int i = tid; i <= g.off.total; i += NT) row[i] = stage[i];
 }
 
 template <int AW>
 constexpr size_t tail_smem() {
-    return (size_t)(2 * 64 * kTP + 6 * kTQ * kTP + kTW * 64 + 2 * kTW + kTQ * (AW + 1) * 64 + kTailLabels) * 4;
+    return (size_t)(2 * 64 * kTP + 6 * kTQ * kTP + kTW * 64 + 2 * kTW + kTQ * (AW + 1) * 64 + kTailLabels + 64 * kTP +
+                    64) * 4;
 }
 
 using TailKernel = void (*)(TailArgs);

@@ -107,3 +107,30 @@ def test_c3_sampled_anchors_bit_exact_vs_oracle(c3):
         for a in range(A):  # every cell's RPE id maps to its count vector w.r.t. anchor a
             want = np.stack([rpes[a].get(int(x), np.zeros(5, np.int32)) for x in cells])
             np.testing.assert_array_equal(tab[ri[b][:, a]], want)
+
+
+def test_c3_fused_encoder_vs_dense_reference(c3):
+    """The fused join+encode kernel at the headline size (lists of ~530
+    distinct landings per anchor, the training batch's query mix) against the
+    dense path (wj_join -> fp32 PyTorch encoder, mode="reference" order),
+    dropout off: logits within 1e-5, gradients within 1e-4 (relative)."""
+    import paper_2202_13538_b200 as wj
+
+    g, s = c3
+    rng = np.random.default_rng(3)
+    n = g.num_nodes
+    seeds = rng.integers(0, n, 48)
+    q = np.stack([rng.choice(seeds, 2, replace=False) for _ in range(96)]).astype(np.int64)
+    y = torch.from_numpy((np.arange(96) < 6).astype(np.float32)).cuda()
+    qd = torch.from_numpy(q).cuda()
+    p = wj.init_params(2, 4, dropout=0.0, seed=21)
+    logits, cache = wj.encoder.forward_fused(p, s, qd, training=False)
+    grads = wj.backward(p, cache, y)
+    dense = wj.dense_batch(s, qd, dtype=torch.float32)
+    logits_r, cache_r = wj.forward(p, dense, training=False, mode="reference")
+    grads_r = wj.backward(p, cache_r, y)
+    lr = logits_r.double()
+    torch.testing.assert_close(logits.double(), lr, rtol=1e-5, atol=1e-5 * float(lr.abs().max()))
+    for k in wj.encoder.TENSOR_ORDER:
+        r = grads_r[k].double()
+        torch.testing.assert_close(grads[k].double(), r, rtol=1e-4, atol=1e-4 * max(float(r.abs().max()), 1e-12))
