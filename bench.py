@@ -218,6 +218,15 @@ def run_ours(args, cfg):
     plan = make_plan(split, index, filt, W + K, BATCH_SEED + rank)
     qd = [torch.from_numpy(q).to(dev) for q, _ in plan]
     yd = [torch.from_numpy(y).to(dev) for _, y in plan]
+    # the planner's per-batch groups of identical queries (wj_group_queries),
+    # resident with their batch
+    from paper_2202_13538_b200.pipeline import GROUP_MAX
+
+    gd = []
+    for q, _ in plan:
+        gb = np.empty(2 * q.shape[0] + 2, dtype=np.int32)
+        _lib.call("wj_group_queries", q.ctypes.data, q.shape[0], q.shape[1], GROUP_MAX, gb.ctypes.data, None)
+        gd.append((torch.from_numpy(gb).to(dev), int(gb[0])))
     B_mean = float(np.mean([q.shape[0] for q, _ in plan[W:]]))
 
     params = wj.init_params(A, L, hidden=64, dropout=0.1, seed=11, device=dev)
@@ -226,7 +235,7 @@ def run_ours(args, cfg):
                         use_graph=True, process_group=(dist.group.WORLD if world > 1 else None),
                         seed=1000 + rank, overlap_inputs=True, launch=args.launch)
     for k in range(W):                       # warm-up: captures every batch shape of the plan
-        step(qd[k], yd[k])
+        step(qd[k], yd[k], groups=gd[k])
     for k in range(W, W + K):
         if step.launch == "graph" and (qd[k].shape[0], A) not in step._graphs:
             step(qd[k], yd[k])
@@ -239,7 +248,7 @@ def run_ours(args, cfg):
         torch.cuda._sleep(2_000_000)
         e0.record()
         for k in range(W, W + K):
-            loss = step(qd[k], yd[k])
+            loss = step(qd[k], yd[k], groups=gd[k])
         e1.record()
         barrier_sync()
     t_step = max_over_ranks(e0.elapsed_time(e1) / 1e3 / K)
@@ -326,7 +335,7 @@ def run_ours(args, cfg):
 
     def e2e_step(k, q, y):
         if chain:
-            step(q, y, loss_out=loss_h[k:k + 1])
+            step(q, y, loss_out=loss_h[k:k + 1], groups=(feeder.groups, feeder.n_groups))
             feeder.consumed()
         else:
             loss_h[k:k + 1].copy_(step(q, y).reshape(1), non_blocking=True)

@@ -243,7 +243,10 @@ int wj_adam(float *params, float *m, float *v, const float *partial, int32_t par
  * mapped pinned host memory (read by the kernels directly; the caller keeps
  * them unchanged until the step completes); loss_out (device or mapped
  * host, may be NULL) receives the step's mean BCE.  Same math and dropout
- * stream as the three separate calls (the TrainStep graph). */
+ * stream as the three separate calls (the TrainStep graph).  groups (device,
+ * from wj_group_queries, needs sched) makes the join+encode kernel schedule
+ * groups of identical queries: a group stages, merges and builds its rows
+ * once and runs tiles + reduction per member -- same outputs. */
 typedef struct wj_stepper wj_stepper;
 int wj_stepper_create(const int64_t *offsets, const int32_t *uniq_x, const int32_t *uniq_id, const int64_t *voff,
                       const int32_t *vcnt, const uint16_t *vslots, const uint16_t *table_rows_f16, int32_t arity,
@@ -253,7 +256,7 @@ int wj_stepper_create(const int64_t *offsets, const int32_t *uniq_x, const int32
                       float beta2, float eps, int64_t *step, float *pooled, float *s_out, float *msum,
                       float *partial, int32_t partial_rows_max, int32_t *sched, wj_stepper **out);
 int wj_stepper_run(wj_stepper *stepper, const int64_t *queries, const float *labels, int64_t n_batch,
-                   float *loss_out, wj_stream_t stream);
+                   const int32_t *groups, int64_t n_groups, float *loss_out, wj_stream_t stream);
 int wj_stepper_destroy(wj_stepper *stepper);
 
 /* Fixed-order column sums out[c] = sum_r partial[r, c] of a [rows, n_cols]
@@ -321,17 +324,27 @@ int wj_planner_get_rng(const wj_planner *planner, uint64_t *words6);
  * labels_out [cap] (1 / 0, may be NULL); n_queries 0 = empty batch. */
 int wj_planner_next(wj_planner *planner, int64_t *queries_out, float *labels_out, int64_t cap,
                     int64_t *n_queries_out, int64_t *n_pos_out, int64_t *n_seeds_out);
+/* Units of identical queries (same anchor tuple, same order) of a batch:
+ * groups_out [2n + 2] int32 = [G | start[0..G] | order[0..n)]; each tuple's
+ * queries in batch order, cut into units of <= max_group members (0 = no
+ * cap), larger units first (stable: first occurrence).  Host only; the
+ * reference's in-seed negatives repeat tuples (~28 % of a C3 batch).  The
+ * producer thread of wj_planner_start_epoch uses max_group = 4. */
+int wj_group_queries(const int64_t *queries, int64_t n, int32_t arity, int32_t max_group, int32_t *groups_out,
+                     int64_t *n_groups_out);
+
 /* One epoch of train()'s batch loop (pipeline.py:287-305) on a producer
  * thread, ahead of the consumer: batches until the positives consumed reach
  * n_pos or a batch is empty, written in order into a caller-owned ring of
  * n_slots slots (ring_queries [n_slots, cap, arity], ring_labels
- * [n_slots, cap], e.g. pinned host memory).  wj_planner_acquire spins until
+ * [n_slots, cap], e.g. pinned host memory; ring_groups [n_slots, 2*cap + 2]
+ * or NULL receives each batch's wj_group_queries).  wj_planner_acquire spins until
  * the next batch is ready and returns its slot (-1 at the end of the epoch,
  * after which the rng state is the reference's end-of-epoch state);
  * wj_planner_release hands a slot back once its contents have been copied.
  * wj_planner_stop abandons the epoch (the rng state is then ahead). */
-int wj_planner_start_epoch(wj_planner *planner, int64_t *ring_queries, float *ring_labels, int32_t n_slots,
-                           int64_t cap);
+int wj_planner_start_epoch(wj_planner *planner, int64_t *ring_queries, float *ring_labels, int32_t *ring_groups,
+                           int32_t n_slots, int64_t cap);
 int wj_planner_acquire(wj_planner *planner, int32_t *slot_out, int64_t *n_queries_out, int64_t *n_pos_out);
 int wj_planner_release(wj_planner *planner, int32_t slot);
 int wj_planner_stop(wj_planner *planner);

@@ -48,7 +48,7 @@ SIGNATURES = {
     "wj_sum_partials": [P, I32, I32, P, P],
     "wj_stepper_create": [P, P, P, P, P, P, P, I32, I32, I32, I32, P, P, P, P, ctypes.c_float, ctypes.c_float, U64,
                           ctypes.c_float, ctypes.c_float, ctypes.c_float, ctypes.c_float, P, P, P, P, P, I32, P, P],
-    "wj_stepper_run": [P, P, P, I64, P, P],
+    "wj_stepper_run": [P, P, P, I64, P, I64, P, P],
     "wj_stepper_destroy": [P],
     "wj_gather_rpe": [P, I64, P, I64, I32, P, I32, P, P],
     "wj_export_dicts": [P, P, P, P, P, I64, I32, I32, P, P, P, P],
@@ -60,7 +60,8 @@ SIGNATURES = {
     "wj_planner_set_rng": [P, P],
     "wj_planner_get_rng": [P, P],
     "wj_planner_next": [P, P, P, I64, P, P, P],
-    "wj_planner_start_epoch": [P, P, P, I32, I64],
+    "wj_planner_start_epoch": [P, P, P, P, I32, I64],
+    "wj_group_queries": [P, I64, I32, I32, P, P],
     "wj_planner_acquire": [P, P, P, P],
     "wj_planner_release": [P, I32],
     "wj_planner_stop": [P],

@@ -76,6 +76,13 @@ struct EncMmaArgs {
     float *s_out;   // [B, AW, 64] or null
     float *msum;    // [B, 64] or null
     int32_t *qsched;  // [2] zeroed query-grab / done counters (dynamic scheduling) or null: static striding
+    // dynamic scheduling over groups of identical queries (null: one query
+    // per unit): [G | start[0..G] | order[0..B)] -- unit u = the queries
+    // order[start[u] .. start[u+1]), all with the same anchor tuple, so the
+    // unit stages, merges and builds its rows once and runs tiles +
+    // reduction per member (each with its own dropout stream and outputs)
+    const int32_t *groups;
+    int64_t n_units;  // G with groups, else n_batch
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -341,10 +348,13 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
     // more queries.  The last CTA to finish resets the counters.
     const bool dyn = g.qsched != nullptr;
     int64_t *next_b = reinterpret_cast<int64_t *>(wscale + 12);
-    auto load_meta1 = [&](int64_t bb, QMeta *dst) {
+    const int32_t *gstart = g.groups ? g.groups + 1 : nullptr;
+    const int32_t *gorder = g.groups ? g.groups + 2 + g.n_units : nullptr;
+    auto load_meta1 = [&](int64_t uu, QMeta *dst) {  // metadata of unit uu's anchor tuple
         if (threadIdx.x < A) {
             QMeta m = {0, 0, 0, 0, 0};
-            if (bb < g.n_batch) {
+            if (uu < g.n_units) {
+                const int64_t bb = gorder ? (int64_t)gorder[gstart[uu]] : uu;
                 const int64_t q = g.queries[bb * A + threadIdx.x];
                 m.lo = g.offsets[q];
                 m.u = (int)(g.offsets[q + 1] - m.lo);
@@ -395,8 +405,11 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
     };
     uint64_t skey = 0;
 
-    int jq = 0;  // local query index
-    for (int64_t b = blockIdx.x; b < g.n_batch; ++jq) {
+    int jq = 0;  // local unit index
+    for (int64_t u = blockIdx.x; u < g.n_units; ++jq) {
+        const int mstart = gorder ? gstart[u] : 0;
+        const int mcount = gorder ? gstart[u + 1] - mstart : 1;
+        int64_t b = gorder ? (int64_t)gorder[mstart] : u;  // the unit's first query
         if (!dyn && jq > 0 && jq % kMetaQ == 0) {  // metadata of the CTA's next kMetaQ queries
             __syncthreads();
             load_meta(b);
@@ -464,9 +477,17 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
             if (dyn) pdl_trigger();
         }
         // last query of this CTA, after the wait: dependents may launch
-        if (!dyn && b + gridDim.x >= g.n_batch) pdl_trigger();
+        if (!dyn && u + gridDim.x >= g.n_units) pdl_trigger();
         if (dyn && threadIdx.x == 0) *next_b = (int64_t)gridDim.x + atomicAdd(g.qsched, 1);
+        int64_t nb = u + gridDim.x;
 
+        for (int mem = 0; mem < mcount; ++mem) {
+        if (mem > 0) {  // the previous member's reduction overlaid the rows: rebuild them
+            b = gorder[mstart + mem];
+            if (threadIdx.x < 2) *reinterpret_cast<uint4 *>(xr + zrow * kRowB + 16 * threadIdx.x) = make_uint4(0, 0, 0, 0);
+            build_rows_x<A, W>(g, threadIdx.x, NT, scr, sid, pu, xr);
+            __syncthreads();
+        }
         // ---- per-warp tiles of 16 virtual landings
         uint32_t qq = (uint32_t)mix64(skey ^ mix64((uint64_t)b));
         qq ^= qq >> 16;
@@ -488,8 +509,7 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
                 tile<false>(vl + v0, xr_s, wt_s, lane, cq, g.t11, 0u, sacc);
         }
         __syncthreads();  // rows are dead: red overlays them
-        int64_t nb = b + gridDim.x;
-        if (dyn) {
+        if (dyn && mem == mcount - 1) {
             nb = *next_b;
             load_meta1(nb, meta + ((jq + 1) & 1) * A);  // lands while the reduction runs
         }
@@ -530,7 +550,8 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
             g.pooled[b * H + m] = s;
         }
         __syncthreads();
-        b = nb;
+        }  // members
+        u = nb;
     }
     if (dyn && threadIdx.x == 0) {
         __threadfence();
@@ -718,6 +739,7 @@ static void fill_args(EncMmaArgs &g, const MmaPlan &pl, const int64_t *queries, 
     g = EncMmaArgs{};
     g.queries = queries;
     g.n_batch = n_batch;
+    g.n_units = n_batch;
     g.offsets = offsets;
     g.ux = uniq_x;
     g.uid = uniq_id;
@@ -866,16 +888,22 @@ extern "C" int wj_stepper_destroy(wj_stepper *st) {
 }
 
 extern "C" int wj_stepper_run(wj_stepper *st, const int64_t *queries, const float *labels, int64_t n_batch,
-                              float *loss_out, wj_stream_t stream) {
+                              const int32_t *groups, int64_t n_groups, float *loss_out, wj_stream_t stream) {
     using namespace wj;
-    if (!st || !queries || !labels || n_batch < 1) {
+    if (!st || !queries || !labels || n_batch < 1 || (groups && (n_groups < 1 || n_groups > n_batch))) {
         set_error("wj_stepper_run: bad arguments");
+        return WJ_ERR_ARG;
+    }
+    if (groups && !st->args.qsched) {
+        set_error("wj_stepper_run: query groups need the dynamic scheduler (sched)");
         return WJ_ERR_ARG;
     }
     EncMmaArgs g = st->args;
     g.queries = queries;
     g.n_batch = n_batch;
-    const int64_t blocks = n_batch < st->plan.slots ? n_batch : st->plan.slots;
+    g.groups = groups;
+    g.n_units = groups ? n_groups : n_batch;
+    const int64_t blocks = g.n_units < st->plan.slots ? g.n_units : st->plan.slots;
     cudaError_t e = launch_pdl(st->plan.k, dim3((unsigned)blocks), dim3(st->plan.nw * 32), st->plan.smem,
                                (cudaStream_t)stream, g);
     if (e != cudaSuccess) {

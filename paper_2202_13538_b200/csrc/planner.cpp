@@ -234,6 +234,10 @@ struct wj_planner {
     std::vector<int64_t> pool;       // optional fixed negative pool [n_pool, arity]
     TupleSet<uint64_t> filter1;  // arity <= 2
     TupleSet<Key2> filter2;      // arity 3-4
+    // grouping of a batch's identical pairs by seed-local ids (the producer
+    // thread): every node of a batch is in its seed set
+    std::vector<int64_t> sset;
+    std::vector<int32_t> sidx, pair_unit, gcnt, gfirst, gmem, gorder;
     Pcg64 rng;
     // per-batch scratch: generation stamps instead of clearing sets
     HugeArray<uint32_t> seed_stamp, batch_stamp;
@@ -251,6 +255,8 @@ struct wj_planner {
     bool running = false;
     int64_t *ring_q = nullptr;
     float *ring_y = nullptr;
+    int32_t *ring_g = nullptr;
+    int32_t group_max = 4;  // unit size of wj_group_queries on the producer thread
     int32_t n_slots = 0;
     int64_t ring_cap = 0, consumed_batches = 0;
     std::unique_ptr<std::atomic<int>[]> slot_ready;
@@ -528,6 +534,104 @@ int64_t negatives(wj_planner *p, int64_t count, int64_t *out) {
 }  // namespace
 
 namespace {
+// Per-thread scratch of wj_group_queries, reused across calls (a call is a
+// few microseconds; allocating and clearing a table each time was 40 us).
+struct GroupScratch {
+    std::vector<Key2> keys;
+    std::vector<uint32_t> stamp;
+    std::vector<int32_t> gid, of, cnt, tstart, members, ustart, usize, ufirst, bucket;
+    uint32_t gen = 0;
+};
+
+void emit_units(GroupScratch &sc, int64_t n, int32_t max_group, int32_t *groups_out) {
+    // each tuple's queries in batch order, cut into units of <= max_group
+    // members (the join+encode kernel runs a unit's members one after the
+    // other in one CTA: a long unit would straggle), larger units first
+    // (counting sort on the unit size, stable)
+    const int32_t T = (int32_t)sc.cnt.size();
+    sc.tstart.assign(T + 1, 0);
+    for (int32_t t = 0; t < T; ++t) sc.tstart[t + 1] = sc.tstart[t] + sc.cnt[t];
+    sc.members.resize(n);
+    sc.cnt.assign(sc.tstart.begin(), sc.tstart.end() - 1);  // reuse as fill pointers
+    for (int64_t i = 0; i < n; ++i) sc.members[sc.cnt[sc.of[i]]++] = (int32_t)i;
+    const int32_t cap_m = max_group > 0 ? max_group : (int32_t)(n > 0 ? n : 1);
+    sc.ufirst.clear();
+    sc.usize.clear();
+    int32_t big = 1;
+    for (int32_t t = 0; t < T; ++t)
+        for (int32_t a = sc.tstart[t]; a < sc.tstart[t + 1]; a += cap_m) {
+            const int32_t sz = std::min(cap_m, sc.tstart[t + 1] - a);
+            sc.ufirst.push_back(a);
+            sc.usize.push_back(sz);
+            big = std::max(big, sz);
+        }
+    const int32_t G = (int32_t)sc.usize.size();
+    sc.bucket.assign(big + 2, 0);  // units per size, then start positions (largest first)
+    for (int32_t g = 0; g < G; ++g) sc.bucket[big - sc.usize[g] + 1]++;
+    for (int32_t b = 1; b <= big + 1; ++b) sc.bucket[b] += sc.bucket[b - 1];
+    sc.ustart.resize(G);
+    for (int32_t g = 0; g < G; ++g) sc.ustart[sc.bucket[big - sc.usize[g]]++] = g;
+    int32_t *start = groups_out + 1, *order = groups_out + 2 + G;
+    groups_out[0] = G;
+    start[0] = 0;
+    for (int32_t r = 0; r < G; ++r) {
+        const int32_t g = sc.ustart[r];
+        start[r + 1] = start[r] + sc.usize[g];
+        for (int32_t k = 0; k < sc.usize[g]; ++k) order[start[r] + k] = sc.members[sc.ufirst[g] + k];
+    }
+}
+
+}  // namespace
+
+extern "C" int wj_group_queries(const int64_t *queries, int64_t n, int32_t arity, int32_t max_group,
+                                int32_t *groups_out, int64_t *n_groups_out) {
+    if (!queries || !groups_out || n < 0 || arity < 1 || arity > 4 || n > 0x3FFFFFFF || max_group < 0) {
+        wj::set_error("wj_group_queries: bad arguments");
+        return arity > 4 ? WJ_ERR_UNSUPPORTED : WJ_ERR_ARG;
+    }
+    static thread_local GroupScratch sc;
+    // ordered tuple -> tuple id (first occurrence order): open addressing
+    // with generation stamps instead of clearing the table
+    uint64_t cap = 16;
+    int cbits = 4;
+    while (cap < (uint64_t)(2 * n)) cap <<= 1, ++cbits;
+    if (sc.keys.size() < cap) {
+        sc.keys.assign(cap, Key2{0, 0});
+        sc.stamp.assign(cap, 0);
+        sc.gid.assign(cap, 0);
+        sc.gen = 0;
+    }
+    if (++sc.gen == 0) {
+        std::fill(sc.stamp.begin(), sc.stamp.end(), 0);
+        sc.gen = 1;
+    }
+    const uint32_t gen = sc.gen;
+    const uint64_t mask = cap - 1;
+    sc.of.resize(n);
+    sc.cnt.clear();
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t *t = queries + i * arity;
+        uint32_t v[4] = {0, 0, 0, 0};
+        for (int a = 0; a < arity; ++a) v[a] = (uint32_t)t[a];
+        const Key2 k{((uint64_t)v[0] << 32) | v[1], ((uint64_t)v[2] << 32) | v[3]};
+        uint64_t h = hash_of(k) >> (64 - cbits);  // top bits: they mix every id
+        while (sc.stamp[h] == gen && !(sc.keys[h] == k)) h = (h + 1) & mask;
+        if (sc.stamp[h] != gen) {
+            sc.stamp[h] = gen;
+            sc.keys[h] = k;
+            sc.gid[h] = (int32_t)sc.cnt.size();
+            sc.cnt.push_back(0);
+        }
+        sc.of[i] = sc.gid[h];
+        sc.cnt[sc.gid[h]]++;
+    }
+    emit_units(sc, n, max_group, groups_out);
+    if (n_groups_out) *n_groups_out = groups_out[0];
+    return WJ_OK;
+}
+
+
+namespace {
 
 // One batch of train() (pipeline.py:292-304) into queries_out / labels_out;
 // on error returns a WJ_ERR_* code with the message in err.
@@ -574,6 +678,57 @@ int plan_one(wj_planner *p, int64_t *queries_out, float *labels_out, int64_t cap
     return WJ_OK;
 }
 
+// Units of identical queries of a just-planned batch, on the producer
+// thread.  Every node of the batch is in its seed set, so for pairs over a
+// small seed set the tuple id comes from a dense (local a, local b) table
+// instead of hashing the tuples; otherwise wj_group_queries.
+void group_planned(wj_planner *p, const int64_t *q, int64_t n, int32_t *out) {
+    const int64_t ns = (int64_t)p->seed_list.size();
+    if (p->arity != 2 || ns > 128 || !p->pool.empty()) {
+        wj_group_queries(q, n, p->arity, p->group_max, out, nullptr);
+        return;
+    }
+    static thread_local GroupScratch sc;
+    int sbits = 4;
+    while ((1ll << sbits) < 2 * ns + 2) ++sbits;
+    const uint64_t smask = ((uint64_t)1 << sbits) - 1;
+    p->sset.assign((size_t)1 << sbits, -1);
+    p->sidx.assign((size_t)1 << sbits, 0);
+    for (int64_t i = 0; i < ns; ++i) {
+        const int64_t a = p->seed_list[i];
+        uint64_t h = hash_of((uint64_t)a) >> (64 - sbits);
+        while (p->sset[h] >= 0) h = (h + 1) & smask;
+        p->sset[h] = a;
+        p->sidx[h] = (int32_t)i;
+    }
+    auto local = [&](int64_t x) -> int32_t {
+        uint64_t h = hash_of((uint64_t)x) >> (64 - sbits);
+        while (p->sset[h] >= 0) {
+            if (p->sset[h] == x) return p->sidx[h];
+            h = (h + 1) & smask;
+        }
+        return -1;
+    };
+    p->pair_unit.assign((size_t)(ns * ns), -1);
+    sc.of.resize(n);
+    sc.cnt.clear();
+    for (int64_t i = 0; i < n; ++i) {
+        const int32_t la = local(q[2 * i]), lb = local(q[2 * i + 1]);
+        if (la < 0 || lb < 0) {  // a positive cut off by the seed-capacity limit
+            wj_group_queries(q, n, p->arity, p->group_max, out, nullptr);
+            return;
+        }
+        int32_t &t = p->pair_unit[(size_t)la * ns + lb];
+        if (t < 0) {
+            t = (int32_t)sc.cnt.size();
+            sc.cnt.push_back(0);
+        }
+        sc.of[i] = t;
+        sc.cnt[t]++;
+    }
+    emit_units(sc, n, p->group_max, out);
+}
+
 // The epoch loop of train() (pipeline.py:287-305): batches until the
 // positives consumed reach len(positives) or a batch comes back empty.
 void epoch_worker(wj_planner *p) {
@@ -596,6 +751,9 @@ void epoch_worker(wj_planner *p) {
             m.n_queries = rc != WJ_OK ? -2 : (npos == 0 ? -1 : nq);
             m.n_pos = npos;
             consumed += npos;
+            if (rc == WJ_OK && nq > 0 && p->ring_g)
+                group_planned(p, p->ring_q + (int64_t)s * p->ring_cap * p->arity, nq,
+                              p->ring_g + (int64_t)s * (2 * p->ring_cap + 2));
         }
         const bool last = m.n_queries < 0;
         p->slot_ready[s].store(1, std::memory_order_release);
@@ -621,8 +779,8 @@ extern "C" int wj_planner_next(wj_planner *p, int64_t *queries_out, float *label
     return rc;
 }
 
-extern "C" int wj_planner_start_epoch(wj_planner *p, int64_t *ring_queries, float *ring_labels, int32_t n_slots,
-                                      int64_t cap) {
+extern "C" int wj_planner_start_epoch(wj_planner *p, int64_t *ring_queries, float *ring_labels, int32_t *ring_groups,
+                                      int32_t n_slots, int64_t cap) {
     if (!p || !ring_queries || !ring_labels || n_slots < 1 || cap < 1) {
         wj::set_error("wj_planner_start_epoch: bad arguments");
         return WJ_ERR_ARG;
@@ -633,6 +791,7 @@ extern "C" int wj_planner_start_epoch(wj_planner *p, int64_t *ring_queries, floa
     }
     p->ring_q = ring_queries;
     p->ring_y = ring_labels;
+    p->ring_g = ring_groups;
     p->n_slots = n_slots;
     p->ring_cap = cap;
     p->consumed_batches = 0;

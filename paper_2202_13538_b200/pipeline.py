@@ -27,6 +27,10 @@ from .store import SubgraphStore
 
 logger = logging.getLogger(__name__)
 
+# largest unit of identical queries the join+encode kernel runs in one CTA
+# (wj_group_queries; the planner's producer thread uses the same)
+GROUP_MAX = 4
+
 
 @dataclass
 class TrainConfig:
@@ -250,6 +254,9 @@ class BatchPlanner:
         self.depth = int(depth)
         self._q = mk(torch.empty((self.depth, self.cap, self.arity), dtype=torch.int64))
         self._y = mk(torch.empty((self.depth, self.cap), dtype=torch.float32))
+        # per slot: groups of identical queries [G | start[0..G] | order] (wj_group_queries)
+        self._g = mk(torch.empty((self.depth, 2 * self.cap + 2), dtype=torch.int32))
+        self.groups_view = None
         self._ev = [None] * self.depth
         self._i = 0
         self._cur = 0
@@ -269,6 +276,8 @@ class BatchPlanner:
         _lib.call("wj_planner_next", self._h, self._q[i].data_ptr(), self._y[i].data_ptr(), self.cap,
                   ctypes.byref(o, 0), ctypes.byref(o, 8), ctypes.byref(o, 16))
         B = int(o[0])
+        _lib.call("wj_group_queries", self._q[i].data_ptr(), B, self.arity, GROUP_MAX, self._g[i].data_ptr(), None)
+        self.groups_view = self._g[i]
         self._cur = i
         return self._q[i][:B], self._y[i][:B], int(o[1])
 
@@ -286,8 +295,8 @@ class BatchPlanner:
         epoch the rng is in the reference's end-of-epoch state."""
         from . import _lib
 
-        _lib.call("wj_planner_start_epoch", self._h, self._q.data_ptr(), self._y.data_ptr(), self.depth,
-                  self.cap)
+        _lib.call("wj_planner_start_epoch", self._h, self._q.data_ptr(), self._y.data_ptr(), self._g.data_ptr(),
+                  self.depth, self.cap)
         self._running = True
         pending = deque()
         slot = ctypes.c_int32()
@@ -311,6 +320,7 @@ class BatchPlanner:
                 B = int(o[0])
                 self._cur = s
                 self._ev[s] = None
+                self.groups_view = self._g[s]
                 yield self._q[s][:B], self._y[s][:B], int(o[1])
                 pending.append((s, self._ev[s]))
                 self._ev[s] = None
@@ -359,6 +369,9 @@ class DeviceFeeder:
     def __init__(self, planner: "BatchPlanner", device, depth: int = 4):
         self.planner, self.dev, self.depth = planner, torch.device(device), int(depth)
         self.q = torch.empty((self.depth, planner.cap, planner.arity), dtype=torch.int64, device=self.dev)
+        self.g = torch.empty((self.depth, 2 * planner.cap + 2), dtype=torch.int32, device=self.dev)
+        self._ng = [0] * self.depth
+        self.groups, self.n_groups = None, 0  # the current batch's query groups (device) and their count
         self._ycache = {}
         self.stream = torch.cuda.Stream(self.dev)
         self.copied = [torch.cuda.Event() for _ in range(self.depth)]
@@ -384,8 +397,12 @@ class DeviceFeeder:
         B = int(q.shape[0])
         if self._used[s]:  # the step that last read this slot
             self.stream.wait_event(self.done[s])
+        gv = self.planner.groups_view
+        G = int(gv[0])
+        self._ng[s] = G
         with torch.cuda.stream(self.stream):
             self.q[s, :B].copy_(q, non_blocking=True)
+            self.g[s, :G + 2 + B].copy_(gv[:G + 2 + B], non_blocking=True)
             self.copied[s].record(self.stream)
         self.planner.release(self.copied[s])  # the pinned slot is free once copied
         return s, B, n_pos
@@ -402,6 +419,7 @@ class DeviceFeeder:
                 nxt = self._issue(b) if b is not None else None
                 self.copied[s].synchronize()  # long complete: issued a step ago
                 self._cur = s
+                self.groups, self.n_groups = self.g[s], self._ng[s]
                 yield self.q[s, :B], self._labels(B, n_pos), n_pos
         finally:
             it.close()
@@ -590,7 +608,7 @@ class TrainStep:
         if self._loss_hist is None:
             self._loss_hist = torch.zeros(self._LOSS_HIST, dtype=torch.float32, device=self.dev)
 
-    def _chain_call(self, q: torch.Tensor, y: torch.Tensor, loss_out=None) -> torch.Tensor:
+    def _chain_call(self, q: torch.Tensor, y: torch.Tensor, loss_out=None, groups=None) -> torch.Tensor:
         from . import _lib
 
         B = q.shape[0]
@@ -606,7 +624,11 @@ class TrainStep:
         i = self._n_calls % self._LOSS_HIST
         self._n_calls += 1
         out = self._loss_hist[i] if loss_out is None else loss_out
-        _lib.call("wj_stepper_run", self._stepper, q.data_ptr(), y.data_ptr(), B, out.data_ptr(),
+        gptr, ng = (None, 0)
+        if groups is not None and self.dynamic_queries:
+            gt, ng = groups
+            gptr = gt.data_ptr()
+        _lib.call("wj_stepper_run", self._stepper, q.data_ptr(), y.data_ptr(), B, gptr, int(ng), out.data_ptr(),
                   _lib.stream_handle(self.dev))
         if (q.device.type == "cpu" or y.device.type == "cpu") and self.record_input_events:
             # host inputs are read in place: their buffers are free once this completes
@@ -630,17 +652,20 @@ class TrainStep:
         except Exception:
             pass
 
-    def __call__(self, q: torch.Tensor, y: torch.Tensor, loss_out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    def __call__(self, q: torch.Tensor, y: torch.Tensor, loss_out: Optional[torch.Tensor] = None,
+                 groups=None) -> torch.Tensor:
         """q: [B, A] int64 ids, y: [B] labels (device, or pinned host for the
         end-to-end path).  Returns the loss (device scalar, valid in stream
         order).  ``launch="chain"``: the inputs are read by the kernels in
         place (pinned host memory stays untouched until the step completes)
         and ``loss_out`` (a one-element device or pinned host tensor)
-        optionally receives the loss instead."""
+        optionally receives the loss instead; ``groups`` = (device int32
+        tensor [G | start | order] from wj_group_queries, G) lets the
+        join+encode kernel share the staging of identical queries."""
         B, A = q.shape
         self._prepare_bc()
         if self.launch == "chain":
-            return self._chain_call(q, y, loss_out)
+            return self._chain_call(q, y, loss_out, groups)
         if not self.use_graph:
             qd, yd = q.to(self.dev, non_blocking=True), y.to(self.dev, self.params.w1.dtype, non_blocking=True)
             self.input_event = torch.cuda.Event()
@@ -829,7 +854,7 @@ def train(store: SubgraphStore, split, cfg: TrainConfig, features=None, train_ne
             # stay in the executor's ring and are summed in blocks
             pending = []
             for q, y, _ in feeder.epoch():
-                pending.append(step(q, y))
+                pending.append(step(q, y, groups=(feeder.groups, feeder.n_groups)))
                 feeder.consumed()
                 n_steps += 1
                 if len(pending) == TrainStep._LOSS_HIST // 2:

@@ -84,3 +84,37 @@ def test_chain_back_to_back_without_syncs(store_and_batches, dynamic):
         outs.append({k: v.clone() for k, v in p.tensors.items()})
     for k in outs[0]:
         assert torch.equal(outs[0][k], outs[1][k]), k
+
+
+def test_chain_with_query_groups_is_bit_identical(store_and_batches):
+    """Scheduling groups of identical queries (shared staging / merge / rows,
+    tiles + reduction per member) gives exactly the ungrouped results; the
+    batches repeat tuples as the reference's in-seed negatives do."""
+    import ctypes
+
+    import paper_2202_13538_b200 as wj
+    from paper_2202_13538_b200 import _lib
+    from paper_2202_13538_b200.pipeline import GROUP_MAX
+
+    store, batches = store_and_batches
+    rng = np.random.default_rng(9)
+    seq = []
+    for q, y in batches[:5]:
+        qq = q.numpy().copy()
+        dup = rng.integers(0, qq.shape[0], size=qq.shape[0] // 2)
+        qq[rng.integers(0, qq.shape[0], size=dup.shape[0])] = qq[dup]  # many repeated tuples
+        gb = np.empty(2 * qq.shape[0] + 2, np.int32)
+        _lib.call("wj_group_queries", qq.ctypes.data, qq.shape[0], 2, GROUP_MAX, gb.ctypes.data, None)
+        assert gb[0] < qq.shape[0]
+        seq.append((torch.from_numpy(qq).cuda(), y.cuda(), (torch.from_numpy(gb).cuda(), int(gb[0]))))
+    outs = []
+    for grouped in (False, True):
+        p = wj.init_params(2, 4, dropout=0.1, seed=3)
+        st = wj.AdamState.for_params(p)
+        step = wj.TrainStep(store, p, st, use_graph=True, seed=5, launch="chain", overlap_inputs=True)
+        losses = [float(step(q, y, groups=g if grouped else None)) for q, y, g in seq]
+        torch.cuda.synchronize()
+        outs.append((losses, {k: v.clone() for k, v in p.tensors.items()}))
+    assert outs[0][0] == outs[1][0]
+    for k in outs[0][1]:
+        assert torch.equal(outs[0][1][k], outs[1][1][k]), k

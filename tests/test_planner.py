@@ -136,3 +136,69 @@ def test_reference_errors():
         BatchPlanner(np.array([[0, 5]]), np.zeros((0, 2)), 3, TrainConfig(), rng, pinned=False)
     with pytest.raises(NotImplementedError):
         BatchPlanner(np.array([[0, 1, 2, 3, 4]]), np.zeros((0, 5)), 6, TrainConfig(), rng, pinned=False)
+
+
+def _check_groups(q, gb, cap=0):
+    """Units: identical ordered tuples, members in batch order, <= cap
+    members (0: a unit is a whole tuple), larger units first, then first
+    occurrence; every query exactly once."""
+    G = int(gb[0])
+    start, order = gb[1:G + 2], gb[G + 2:G + 2 + q.shape[0]]
+    sizes = np.diff(start)
+    assert start[0] == 0 and start[-1] == q.shape[0] and np.all(sizes > 0)
+    assert sorted(order.tolist()) == list(range(q.shape[0]))
+    assert np.all(np.diff(sizes) <= 0)
+    if cap:
+        assert sizes.max() <= cap
+    seen = {}
+    for g in range(G):
+        mem = order[start[g]:start[g + 1]]
+        assert np.all(np.diff(mem) > 0)  # batch order inside a unit
+        t = tuple(q[mem[0]])
+        assert all(tuple(q[i]) == t for i in mem)
+        if not cap:
+            assert t not in seen
+        seen.setdefault(t, []).append(g)
+    for s in np.unique(sizes):  # equal-size units: by their tuple's first occurrence, then chunk
+        firsts = [min(order[start[h]] for h in seen[tuple(q[order[start[g]]])]) for g in range(G) if sizes[g] == s]
+        assert firsts == sorted(firsts)
+    if not cap:
+        assert G == len({tuple(r) for r in q.tolist()})
+    else:
+        counts = {}
+        for r in q.tolist():
+            counts[tuple(r)] = counts.get(tuple(r), 0) + 1
+        assert G == sum(-(-c // cap) for c in counts.values())
+
+
+def test_group_queries():
+    """wj_group_queries: identical ordered tuples grouped, first-occurrence
+    order, members in batch order; (a, b) and (b, a) are different."""
+    import ctypes
+
+    from paper_2202_13538_b200 import _lib
+
+    rng = np.random.default_rng(0)
+    for A in (1, 2, 3, 4):
+        for n in (1, 7, 500):
+            q = rng.integers(0, 6, size=(n, A)).astype(np.int64)
+            for cap in (0, 1, 2, 3):
+                gb = np.empty(2 * n + 2, np.int32)
+                ng = ctypes.c_int64()
+                _lib.call("wj_group_queries", q.ctypes.data, n, A, cap, gb.ctypes.data, ctypes.byref(ng))
+                assert ng.value == gb[0]
+                _check_groups(q, gb, cap)
+
+
+@pytest.mark.parametrize("name", CASES[:2])
+def test_planner_emits_groups(name):
+    d = _load(name)
+    bp = _planner(d, _rng(d))
+    from paper_2202_13538_b200.pipeline import GROUP_MAX
+
+    for q, y, _ in bp.epoch():
+        _check_groups(q.numpy(), bp.groups_view.numpy(), GROUP_MAX)
+    bp.close()
+    bp = _planner(d, _rng(d))
+    q, y, _ = bp.next()
+    _check_groups(q.numpy(), bp.groups_view.numpy(), GROUP_MAX)
