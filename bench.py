@@ -279,6 +279,9 @@ def run_ours(args, cfg):
     t_enc = None
     if A * (L + 1) <= 16:
         def enc_launch(k):
+            if step.launch == "chain":  # the production kernel: dynamic scheduling over query groups
+                step.encode_only(qd[k], groups=gd[k])
+                return
             b = enc_bufs[qd[k].shape[0]]
             t = params.tensors
             wj.encoder.join_encode(store, qd[k], t["w1"], t["b1"], 0.9, 5, step_t, b["pooled"], b["S"],

@@ -257,6 +257,11 @@ int wj_stepper_create(const int64_t *offsets, const int32_t *uniq_x, const int32
                       float *partial, int32_t partial_rows_max, int32_t *sched, wj_stepper **out);
 int wj_stepper_run(wj_stepper *stepper, const int64_t *queries, const float *labels, int64_t n_batch,
                    const int32_t *groups, int64_t n_groups, float *loss_out, wj_stream_t stream);
+/* The step's join+encode kernel alone, exactly as wj_stepper_run launches
+ * it (same plan, scheduling and buffers; the step counter is not advanced):
+ * for timing the production kernel in isolation. */
+int wj_stepper_encode(wj_stepper *stepper, const int64_t *queries, int64_t n_batch, const int32_t *groups,
+                      int64_t n_groups, wj_stream_t stream);
 int wj_stepper_destroy(wj_stepper *stepper);
 
 /* Fixed-order column sums out[c] = sum_r partial[r, c] of a [rows, n_cols]

@@ -887,15 +887,15 @@ extern "C" int wj_stepper_destroy(wj_stepper *st) {
     return WJ_OK;
 }
 
-extern "C" int wj_stepper_run(wj_stepper *st, const int64_t *queries, const float *labels, int64_t n_batch,
-                              const int32_t *groups, int64_t n_groups, float *loss_out, wj_stream_t stream) {
+extern "C" int wj_stepper_encode(wj_stepper *st, const int64_t *queries, int64_t n_batch, const int32_t *groups,
+                                 int64_t n_groups, wj_stream_t stream) {
     using namespace wj;
-    if (!st || !queries || !labels || n_batch < 1 || (groups && (n_groups < 1 || n_groups > n_batch))) {
-        set_error("wj_stepper_run: bad arguments");
+    if (!st || !queries || n_batch < 1 || (groups && (n_groups < 1 || n_groups > n_batch))) {
+        set_error("wj_stepper_encode: bad arguments");
         return WJ_ERR_ARG;
     }
     if (groups && !st->args.qsched) {
-        set_error("wj_stepper_run: query groups need the dynamic scheduler (sched)");
+        set_error("wj_stepper_encode: query groups need the dynamic scheduler (sched)");
         return WJ_ERR_ARG;
     }
     EncMmaArgs g = st->args;
@@ -907,9 +907,26 @@ extern "C" int wj_stepper_run(wj_stepper *st, const int64_t *queries, const floa
     cudaError_t e = launch_pdl(st->plan.k, dim3((unsigned)blocks), dim3(st->plan.nw * 32), st->plan.smem,
                                (cudaStream_t)stream, g);
     if (e != cudaSuccess) {
-        set_error("wj_stepper_run: join_encode launch: %s", cudaGetErrorString(e));
+        set_error("wj_stepper: join_encode launch: %s", cudaGetErrorString(e));
         return WJ_ERR_CUDA;
     }
+    return check_launch("wj_stepper_encode");
+}
+
+extern "C" int wj_stepper_run(wj_stepper *st, const int64_t *queries, const float *labels, int64_t n_batch,
+                              const int32_t *groups, int64_t n_groups, float *loss_out, wj_stream_t stream) {
+    using namespace wj;
+    if (!st || !queries || !labels || n_batch < 1 || (groups && (n_groups < 1 || n_groups > n_batch))) {
+        set_error("wj_stepper_run: bad arguments");
+        return WJ_ERR_ARG;
+    }
+    if (groups && !st->args.qsched) {
+        set_error("wj_stepper_run: query groups need the dynamic scheduler (sched)");
+        return WJ_ERR_ARG;
+    }
+    const int rc0 = wj_stepper_encode(st, queries, n_batch, groups, n_groups, stream);
+    if (rc0 != WJ_OK) return rc0;
+    EncMmaArgs g = st->args;
     int64_t rows = (n_batch + 15) / 16;
     if (rows > st->tail_rows_max) rows = st->tail_rows_max;
     int rc = wj_encoder_tail(g.pooled, g.s_out, g.msum, labels, n_batch, st->aw, 64, st->params, st->offsets9,

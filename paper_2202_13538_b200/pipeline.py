@@ -642,6 +642,21 @@ class TrainStep:
         self.params.version += 1
         return out
 
+    def encode_only(self, q: torch.Tensor, groups=None) -> None:
+        """Chain mode: launch just this step's join+encode kernel (same
+        plan, scheduling and buffers; the step counter is not advanced)."""
+        from . import _lib
+
+        if self.launch != "chain":
+            raise ValueError("encode_only needs launch='chain'")
+        if self._stepper is None or q.shape[0] > self._stepper_cap:
+            self._make_stepper(q.shape[0])
+        gptr, ng = (None, 0)
+        if groups is not None and self.dynamic_queries:
+            gptr, ng = groups[0].data_ptr(), int(groups[1])
+        _lib.call("wj_stepper_encode", self._stepper, q.data_ptr(), q.shape[0], gptr, ng,
+                  _lib.stream_handle(self.dev))
+
     def __del__(self):
         try:
             if getattr(self, "_stepper", None) is not None:

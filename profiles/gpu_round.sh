@@ -11,7 +11,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; head -c 300 gpurun_out/bench_$TAG.json; echo
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref_$TAG.json 2> gpurun_out/bench_ref_$TAG.err; head -c 300 gpurun_out/bench_ref_$TAG.json; echo
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:join_encode -s 1 -c 1 -o gpurun_out/enc_$TAG -f python profiles/kernel_driver.py --config c3 --what enc --reps 3 > gpurun_out/ncu_enc_$TAG.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k "regex:tail_tc|adam" -s 2 -c 2 -o gpurun_out/tail_$TAG -f python profiles/kernel_driver.py --config c3 --what step --reps 3 > gpurun_out/ncu_tail_$TAG.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:join_encode -s 2 -c 1 -o gpurun_out/enc_$TAG -f python profiles/kernel_driver.py --config c3 --what chain --reps 4 > gpurun_out/ncu_enc_$TAG.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k "regex:tail_tc|adam" -s 2 -c 2 -o gpurun_out/tail_$TAG -f python profiles/kernel_driver.py --config c3 --what chain --reps 4 > gpurun_out/ncu_tail_$TAG.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k "regex:rpe_kernel|sample_walks|intern|vindex" -o gpurun_out/pre_$TAG -f python profiles/kernel_driver.py --config c3 --what preprocess > gpurun_out/ncu_pre_$TAG.log 2>&1
 ls -la gpurun_out | tail -30

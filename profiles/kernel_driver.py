@@ -3,6 +3,8 @@
     ncu ... python profiles/kernel_driver.py --config c2 --what preprocess
     ncu ... python profiles/kernel_driver.py --config c3 --what join --reps 3
     ncu ... python profiles/kernel_driver.py --config c3 --what step --reps 3
+    ncu ... python profiles/kernel_driver.py --config c3 --what chain --reps 4   (the bench's step
+        executor: dynamic scheduling over query groups)
 """
 
 import argparse
@@ -23,7 +25,7 @@ from paper_2202_13538_b200.joiner import dense_batch  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c3")
-    ap.add_argument("--what", default="join", choices=["preprocess", "join", "step", "enc"])
+    ap.add_argument("--what", default="join", choices=["preprocess", "join", "step", "enc", "chain"])
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--dense", default="float32")
     ap.add_argument("--mode", default="fused")
@@ -47,6 +49,17 @@ def main():
         step_t = torch.zeros(1, dtype=torch.int64, device=dev)
         for q in qd:
             wj.encoder.forward_fused(p, store, q, training=True, seed=3, step=step_t)
+    elif a.what == "chain":
+        from paper_2202_13538_b200 import _lib
+        from paper_2202_13538_b200.pipeline import GROUP_MAX
+
+        p = wj.init_params(2, cfg["L"], dropout=0.1, seed=11, device=dev)
+        st = wj.AdamState.for_params(p)
+        step = wj.TrainStep(store, p, st, use_graph=True, launch="chain", seed=3)
+        for (q, _), qq, y in zip(plan, qd, yd):
+            gb = np.empty(2 * q.shape[0] + 2, dtype=np.int32)
+            _lib.call("wj_group_queries", q.ctypes.data, q.shape[0], q.shape[1], GROUP_MAX, gb.ctypes.data, None)
+            step(qq, y, groups=(torch.from_numpy(gb).to(dev), int(gb[0])))
     else:
         p = wj.init_params(2, cfg["L"], dropout=0.1, seed=11, device=dev)
         st = wj.AdamState.for_params(p)
