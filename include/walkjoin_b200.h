@@ -262,6 +262,14 @@ int wj_stepper_run(wj_stepper *stepper, const int64_t *queries, const float *lab
  * for timing the production kernel in isolation. */
 int wj_stepper_encode(wj_stepper *stepper, const int64_t *queries, int64_t n_batch, const int32_t *groups,
                       int64_t n_groups, wj_stream_t stream);
+/* Data parallel: the step split around the gradient exchange.
+ * wj_stepper_grads = join+encode + tail + fixed-order sum of the partial
+ * rows into grad_out [n_params + 1] (gradients | loss); the caller
+ * all-reduces (averages) it over ranks, then wj_stepper_apply runs Adam on
+ * it (and writes the loss to loss_out, device or mapped host, may be NULL). */
+int wj_stepper_grads(wj_stepper *stepper, const int64_t *queries, const float *labels, int64_t n_batch,
+                     const int32_t *groups, int64_t n_groups, float *grad_out, wj_stream_t stream);
+int wj_stepper_apply(wj_stepper *stepper, const float *grad, float *loss_out, wj_stream_t stream);
 int wj_stepper_destroy(wj_stepper *stepper);
 
 /* Fixed-order column sums out[c] = sum_r partial[r, c] of a [rows, n_cols]

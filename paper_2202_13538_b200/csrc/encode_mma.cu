@@ -936,6 +936,38 @@ extern "C" int wj_stepper_run(wj_stepper *st, const int64_t *queries, const floa
                    st->eps, st->step, nullptr, loss_out, stream);
 }
 
+// Data parallel: the step split around the gradient exchange -- join+encode
+// and tail, then the fixed-order sum of the partial rows into grad_out
+// [n_params + 1] (gradients | loss); the caller all-reduces (averages) it
+// and wj_stepper_apply runs Adam on it.
+extern "C" int wj_stepper_grads(wj_stepper *st, const int64_t *queries, const float *labels, int64_t n_batch,
+                                const int32_t *groups, int64_t n_groups, float *grad_out, wj_stream_t stream) {
+    using namespace wj;
+    if (!st || !queries || !labels || !grad_out || n_batch < 1) {
+        set_error("wj_stepper_grads: bad arguments");
+        return WJ_ERR_ARG;
+    }
+    const int rc0 = wj_stepper_encode(st, queries, n_batch, groups, n_groups, stream);
+    if (rc0 != WJ_OK) return rc0;
+    EncMmaArgs g = st->args;
+    int64_t rows = (n_batch + 15) / 16;
+    if (rows > st->tail_rows_max) rows = st->tail_rows_max;
+    int rc = wj_encoder_tail(g.pooled, g.s_out, g.msum, labels, n_batch, st->aw, 64, st->params, st->offsets9,
+                             st->scale, nullptr, st->partial, (int32_t)rows, nullptr, st->step, stream);
+    if (rc != WJ_OK) return rc;
+    return wj_sum_partials(st->partial, (int32_t)rows, st->n_params + 1, grad_out, stream);
+}
+
+extern "C" int wj_stepper_apply(wj_stepper *st, const float *grad, float *loss_out, wj_stream_t stream) {
+    using namespace wj;
+    if (!st || !grad) {
+        set_error("wj_stepper_apply: bad arguments");
+        return WJ_ERR_ARG;
+    }
+    return wj_adam(st->params, st->m, st->v, grad, 1, st->n_params, st->lr, st->beta1, st->beta2, st->eps, st->step,
+                   nullptr, loss_out, stream);
+}
+
 
 extern "C" int wj_join_cross(const int64_t *queries, int64_t n_batch, int32_t arity, const int64_t *offsets,
                              const int32_t *uniq_x, const int32_t *uniq_id, int32_t max_unique, int32_t *cross_out,

@@ -489,7 +489,7 @@ class TrainStep:
             raise ValueError(f"launch must be 'graph' or 'chain', got {launch!r}")
         # "chain": the native step executor (wj_stepper_*): three programmatic-
         # dependent launches per step, consecutive steps chained on the stream
-        self.launch = launch if (self.fast_tail and process_group is None) else "graph"
+        self.launch = launch if self.fast_tail else "graph"
         self._stepper = None
         self._stepper_cap = 0
         # chain mode: the join+encode kernel grabs queries from a device counter
@@ -628,8 +628,17 @@ class TrainStep:
         if groups is not None and self.dynamic_queries:
             gt, ng = groups
             gptr = gt.data_ptr()
-        _lib.call("wj_stepper_run", self._stepper, q.data_ptr(), y.data_ptr(), B, gptr, int(ng), out.data_ptr(),
-                  _lib.stream_handle(self.dev))
+        sh = _lib.stream_handle(self.dev)
+        if self.group is None:
+            _lib.call("wj_stepper_run", self._stepper, q.data_ptr(), y.data_ptr(), B, gptr, int(ng), out.data_ptr(),
+                      sh)
+        else:  # data parallel: grads + loss -> NCCL average -> Adam
+            from .distributed import all_reduce_mean
+
+            _lib.call("wj_stepper_grads", self._stepper, q.data_ptr(), y.data_ptr(), B, gptr, int(ng),
+                      _lib.ptr(self.grad_flat), sh)
+            all_reduce_mean(self.grad_flat, self.group)
+            _lib.call("wj_stepper_apply", self._stepper, _lib.ptr(self.grad_flat), out.data_ptr(), sh)
         if (q.device.type == "cpu" or y.device.type == "cpu") and self.record_input_events:
             # host inputs are read in place: their buffers are free once this completes
             if not hasattr(self, "_events"):

@@ -47,7 +47,11 @@ def test_sharded_preprocess_equals_single(nccl_group):
     assert np.array_equal(a.dict_vals, b.dict_vals)
 
 
-def test_dp_fused_step_equals_single(nccl_group):
+@pytest.mark.parametrize("launch", ["graph", "chain"])
+def test_dp_fused_step_equals_single(nccl_group, launch):
+    """graph: the all-reduce is captured in the step graph; chain: the step
+    executor split around it (wj_stepper_grads -> NCCL average ->
+    wj_stepper_apply)."""
     import paper_2202_13538_b200 as wj
 
     rng = np.random.default_rng(5)
@@ -59,8 +63,8 @@ def test_dp_fused_step_equals_single(nccl_group):
     for group in (None, nccl_group):
         p = wj.init_params(2, 4, dropout=0.1, seed=3)
         st = wj.AdamState.for_params(p)
-        step = wj.TrainStep(s, p, st, mode="fused", seed=12, use_graph=True, process_group=group)
-        assert step.fast_tail
+        step = wj.TrainStep(s, p, st, mode="fused", seed=12, use_graph=True, process_group=group, launch=launch)
+        assert step.fast_tail and step.launch == launch
         losses = [float(step(q, y)) for _ in range(4)]
         out.append((losses, {k: v.clone() for k, v in p.tensors.items()}))
     assert out[0][0] == out[1][0]
