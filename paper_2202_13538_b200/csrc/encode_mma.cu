@@ -525,29 +525,29 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
                     if (c <= AW) myred[(16 * mt + gq + 8 * (r >> 1)) * kRedS + c] = sacc[mt][nt][r];
                 }
         __syncthreads();
-        // column sums in a fixed order (G carries a factor 2: halve); S^T[h][c]
-        // for c <= AW stays in warp 0's slot
-        for (int i = threadIdx.x; i < (AW + 1) * H; i += NT) {
-            const int c = i / H, m = i - c * H;
-            float s = 0.f;
-#pragma unroll
-            for (int w = 0; w < kMW; ++w) s += red[w * H * kRedS + m * kRedS + c];
-            s *= 0.5f;
-            if (c < AW) {
-                if (g.s_out) g.s_out[(b * AW + c) * (int64_t)H + m] = s;
-            } else if (g.msum) {
-                g.msum[b * H + m] = s;
-            }
-            red[m * kRedS + c] = s;  // warp 0's slot: only this thread read it
-        }
-        __syncthreads();
-        // pooled[h] = sum_c W1aug[c][h] S^T[h][c]  (relu(z) * kept = z * kept)
+        // one thread per unit: column sums in a fixed order (G carries a factor
+        // 2: halve), then pooled[h] = sum_c W1aug[c][h] S^T[h][c] (relu(z) *
+        // kept = z * kept) in the same thread -- no barrier between them
         if (threadIdx.x < H) {
             const int m = threadIdx.x;
-            float s = g.b1[m] * red[m * kRedS + AW];
+            float sv[AW + 1];
 #pragma unroll
-            for (int c = 0; c < AW; ++c) s = fmaf(g.w1[c * H + m], red[m * kRedS + c], s);
-            g.pooled[b * H + m] = s;
+            for (int c = 0; c <= AW; ++c) {
+                float s = 0.f;
+#pragma unroll
+                for (int w = 0; w < kMW; ++w) s += red[w * H * kRedS + m * kRedS + c];
+                s *= 0.5f;
+                sv[c] = s;
+                if (c < AW) {
+                    if (g.s_out) g.s_out[(b * AW + c) * (int64_t)H + m] = s;
+                } else if (g.msum) {
+                    g.msum[b * H + m] = s;
+                }
+            }
+            float pv = g.b1[m] * sv[AW];
+#pragma unroll
+            for (int c = 0; c < AW; ++c) pv = fmaf(g.w1[c * H + m], sv[c], pv);
+            g.pooled[b * H + m] = pv;
         }
         __syncthreads();
         }  // members
