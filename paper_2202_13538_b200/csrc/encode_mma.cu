@@ -444,12 +444,23 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
                     for (int i = threadIdx.x; i < U[a]; i += NT) cp_async4(scr + (a * (A - 1) + jj) * mu + i, gc + i);
                 }
         }
+        // the anchors' virtual-landing lists (uint16, anchor-local) with the
+        // anchor's row offset added: 4 loads in flight per thread
 #pragma unroll
         for (int a = 0; a < A; ++a) {
             const uint16_t *vs = g.vslots + qm[a].vo;
             const uint16_t add = (uint16_t)(a * mu);
-            for (int i = threadIdx.x; i < V2[a]; i += NT) vl[p2[a] + i] = (uint16_t)(__ldg(vs + i) + add);
-            for (int i = threadIdx.x; i < V1[a]; i += NT) vl[P2 + p1[a] + i] = (uint16_t)(__ldg(vs + V2[a] + i) + add);
+            const int n2 = V2[a], nall = V2[a] + V1[a];
+            for (int i0 = threadIdx.x; i0 < nall; i0 += 4 * NT) {
+                uint16_t v[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) v[k] = i0 + k * NT < nall ? __ldg(vs + i0 + k * NT) : (uint16_t)0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int i = i0 + k * NT;
+                    if (i < nall) vl[i < n2 ? p2[a] + i : P2 + p1[a] + (i - n2)] = (uint16_t)(v[k] + add);
+                }
+            }
         }
         for (int i = p2[A] + threadIdx.x; i < P2; i += NT) vl[i] = (uint16_t)zrow;
         for (int i = P2 + p1[A] + threadIdx.x; i < P2 + P1; i += NT) vl[i] = (uint16_t)zrow;
