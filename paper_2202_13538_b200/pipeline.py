@@ -12,6 +12,7 @@ from __future__ import annotations
 import ctypes
 import logging
 import os
+import threading
 import time
 from collections import deque
 from dataclasses import dataclass, field
@@ -232,7 +233,7 @@ class BatchPlanner:
     (B = 0: empty batch)."""
 
     def __init__(self, positives, filter_rows, num_nodes: int, cfg: TrainConfig, rng: np.random.Generator,
-                 pool=None, depth: int = 4, pinned: bool = True):
+                 pool=None, depth: int = 4, pinned: bool = True, background: bool = False):
         from . import _lib
 
         pos = np.ascontiguousarray(positives, dtype=np.int64)
@@ -243,13 +244,29 @@ class BatchPlanner:
         self._lib = _lib.load()
         self.rng, self.arity = rng, int(pos.shape[1])
         self.cap = int(cfg.batch_size) * (1 + int(cfg.k_neg))
-        h = ctypes.c_void_p()
-        _lib.call("wj_planner_create", pos.ctypes.data, pos.shape[0], self.arity, filt.ctypes.data,
-                  filt.shape[0], int(num_nodes), int(cfg.batch_capacity), int(cfg.batch_size), int(cfg.k_neg),
-                  None if pl is None else pl.ctypes.data, 0 if pl is None else pl.shape[0], ctypes.byref(h))
-        self._h = h
+        self._h = ctypes.c_void_p()
+        cargs = (pos.ctypes.data, pos.shape[0], self.arity, filt.ctypes.data, filt.shape[0], int(num_nodes),
+                 int(cfg.batch_capacity), int(cfg.batch_size), int(cfg.k_neg),
+                 None if pl is None else pl.ctypes.data, 0 if pl is None else pl.shape[0], ctypes.byref(self._h))
         self._words = _rng_words(rng)
-        _lib.call("wj_planner_set_rng", self._h, self._words.ctypes.data)
+        self._builder, self._build_err = None, None
+        if background:
+            # the build (query index + positive-tuple set, ~0.15 s at C3) runs on
+            # a host thread -- ctypes releases the GIL -- e.g. while the device
+            # preprocess runs; the first use waits for it
+            self._keep = (pos, filt, pl)
+
+            def build():
+                try:
+                    _lib.call("wj_planner_create", *cargs)
+                except BaseException as e:  # re-raised by wait()
+                    self._build_err = e
+
+            self._builder = threading.Thread(target=build, name="wj-planner-build", daemon=True)
+            self._builder.start()
+        else:
+            _lib.call("wj_planner_create", *cargs)
+            _lib.call("wj_planner_set_rng", self._h, self._words.ctypes.data)
         mk = (lambda t: t.pin_memory()) if pinned and torch.cuda.is_available() else (lambda t: t)
         self.depth = int(depth)
         self._q = mk(torch.empty((self.depth, self.cap, self.arity), dtype=torch.int64))
@@ -263,10 +280,23 @@ class BatchPlanner:
         self._running = False
         self._out = (ctypes.c_int64 * 3)()
 
+    def wait(self) -> None:
+        """Block until a background build has finished (no-op otherwise)."""
+        from . import _lib
+
+        if self._builder is not None:
+            self._builder.join()
+            self._builder = None
+            self._keep = None
+            if self._build_err is not None:
+                raise self._build_err
+            _lib.call("wj_planner_set_rng", self._h, self._words.ctypes.data)
+
     def next(self):
         """One batch, planned on the calling thread."""
         from . import _lib
 
+        self.wait()
         i = self._i
         self._i = (i + 1) % self.depth
         if self._ev[i] is not None:  # the copy that last read this buffer
@@ -295,6 +325,7 @@ class BatchPlanner:
         epoch the rng is in the reference's end-of-epoch state."""
         from . import _lib
 
+        self.wait()
         _lib.call("wj_planner_start_epoch", self._h, self._q.data_ptr(), self._y.data_ptr(), self._g.data_ptr(),
                   self.depth, self.cap)
         self._running = True
@@ -333,6 +364,7 @@ class BatchPlanner:
         """Write the planner's PCG64 state back into the numpy generator."""
         from . import _lib
 
+        self.wait()
         _lib.call("wj_planner_get_rng", self._h, self._words.ctypes.data)
         w = [int(x) for x in self._words]
         st = self.rng.bit_generator.state
@@ -341,6 +373,7 @@ class BatchPlanner:
         self.rng.bit_generator.state = st
 
     def close(self) -> None:
+        self.wait()
         if getattr(self, "_h", None) is not None and self._h.value:
             if not self._running:
                 self.sync()

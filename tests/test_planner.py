@@ -202,3 +202,22 @@ def test_planner_emits_groups(name):
     bp = _planner(d, _rng(d))
     q, y, _ = bp.next()
     _check_groups(q.numpy(), bp.groups_view.numpy(), GROUP_MAX)
+
+
+def test_background_build_same_batches():
+    """BatchPlanner(background=True) builds on a host thread; the first use
+    waits for it and the batches are the same."""
+    d = _load(CASES[0])
+    from paper_2202_13538_b200.pipeline import BatchPlanner, TrainConfig
+
+    cfg = TrainConfig(batch_capacity=int(d["batch_capacity"]), batch_size=int(d["batch_size"]),
+                      k_neg=int(d["k_neg"]), seed=int(d["seed"]))
+    filt = np.concatenate([d["positives"], d["filter_extra"]])
+    a = BatchPlanner(d["positives"], filt, int(d["num_nodes"]), cfg, _rng(d), pinned=False)
+    b = BatchPlanner(d["positives"], filt, int(d["num_nodes"]), cfg, _rng(d), pinned=False, background=True)
+    for _ in range(5):
+        qa, ya, _ = a.next()
+        qb, yb, _ = b.next()
+        assert np.array_equal(qa.numpy(), qb.numpy()) and np.array_equal(ya.numpy(), yb.numpy())
+    a.close()
+    b.close()
