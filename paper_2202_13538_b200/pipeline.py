@@ -884,22 +884,25 @@ def train(store: SubgraphStore, split, cfg: TrainConfig, features=None, train_ne
             raise ValueError(f"feature matrix has {features.shape[0]} rows for {store.num_nodes} nodes")
     feature_dim = 0 if features is None else int(features.shape[1])
     dev = store.device
+    filt_rows = [positives] + [_rows(g) for g in (split.valid_pos, split.test_pos) if len(g)]
+    batch_rng = np.random.default_rng(derive_seed(cfg.seed, "minibatch"))
+    pool = _rows(train_negatives) if train_negatives is not None and len(train_negatives) else None
+    planner = feeder = index = pos_filter = None
+    if native_planner and arity <= 4:
+        # built on a host thread while the model and the step executor are set up
+        planner = BatchPlanner(positives, np.concatenate(filt_rows), store.num_nodes, cfg, batch_rng, pool=pool,
+                               background=True)
+        feeder = DeviceFeeder(planner, dev)
+    else:  # Python planning: the reference's structures
+        index = QueryOverlapIndex(positives)
+        pos_filter = PositiveFilter(np.concatenate(filt_rows), store.num_nodes)
     params = E.init_params(arity, store.walk_steps, hidden=cfg.hidden_dim, feature_dim=feature_dim,
                            dropout=cfg.dropout, seed=derive_seed(cfg.seed, "init"), device=dev)
     state = E.AdamState.for_params(params, lr=cfg.lr)
-    index = QueryOverlapIndex(positives)
-    filt_rows = [positives] + [_rows(g) for g in (split.valid_pos, split.test_pos) if len(g)]
-    pos_filter = PositiveFilter(np.concatenate(filt_rows), store.num_nodes)
-    batch_rng = np.random.default_rng(derive_seed(cfg.seed, "minibatch"))
-    pool = _rows(train_negatives) if train_negatives is not None and len(train_negatives) else None
     feats_d = None if features is None else torch.as_tensor(features, dtype=torch.float32, device=dev)
     step = TrainStep(store, params, state, mode="fused" if feats_d is None else "pooled",
                      use_graph=use_graph, seed=derive_seed(cfg.seed, "dropout"), features=feats_d,
                      launch="chain" if use_graph else "graph")
-    planner = feeder = None
-    if native_planner and arity <= 4:
-        planner = BatchPlanner(positives, np.concatenate(filt_rows), store.num_nodes, cfg, batch_rng, pool=pool)
-        feeder = DeviceFeeder(planner, dev)
     history = []
     best_params, best_metric, best_epoch = params.copy(), -np.inf, 0
     for epoch in range(1, cfg.max_epochs + 1):
