@@ -446,14 +446,20 @@ class DeviceFeeder:
         try:
             b = next(it, None)
             nxt = self._issue(b) if b is not None else None
+            first = True
             while nxt is not None:
                 s, B, n_pos = nxt
-                b = next(it, None)
-                nxt = self._issue(b) if b is not None else None
+                if not first:  # the next batch's copy goes out before this one is handed over
+                    b = next(it, None)
+                    nxt = self._issue(b) if b is not None else None
                 self.copied[s].synchronize()  # long complete: issued a step ago
                 self._cur = s
                 self.groups, self.n_groups = self.g[s], self._ng[s]
                 yield self.q[s, :B], self._labels(B, n_pos), n_pos
+                if first:  # the first batch is handed over as soon as it is copied
+                    first = False
+                    b = next(it, None)
+                    nxt = self._issue(b) if b is not None else None
         finally:
             it.close()
 
