@@ -58,6 +58,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--cpu-shard-nodes", type=int, default=0, help="0 = auto")
+    ap.add_argument("--pre", default="sharded", choices=["sharded", "redundant"],
+                    help="N>1 preprocess: node-range shards + NCCL all-gathers, or the full store on every rank "
+                         "(no communication; SURVEY 8(e) asks for both)")
     ap.add_argument("--launch", default="chain", choices=["chain", "graph"],
                     help="chain: native step executor, PDL-chained across steps; graph: one CUDA graph per step")
     ap.add_argument("--mode", default="fused", choices=["fused", "pooled", "reference"],
@@ -196,7 +199,7 @@ def run_ours(args, cfg):
     g = split.walk_graph
 
     # ---- preprocess: warm once, then time the full Alg. 1 on device
-    if world > 1:
+    if world > 1 and args.pre == "sharded":
         from paper_2202_13538_b200.distributed import preprocess_sharded as prep
     else:
         prep = wj.preprocess
@@ -474,6 +477,7 @@ def run_ours(args, cfg):
             "final_loss": final_loss,
             "parallelism": f"dp{world}",
             "launch": step.launch,
+            "preprocess": args.pre if world > 1 else "single",
         },
         "e2e": {"value": round(e2e, 1), "unit": "queries/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": 4, "t_pre_ms": round(t_pre_e2e * 1e3, 3),
