@@ -640,7 +640,11 @@ def run_reference(args, cfg):
     adam = encoder_ref.Adam(params)
     rng_ref = np.random.default_rng(BATCH_SEED)
     drop_rng = np.random.default_rng(5)
+    # per-step sample bounded so the whole --steps K --warmup W run stays
+    # within about a minute of encoder time (the fp64 encoder is ~1.8 s per
+    # 408 queries at C3): 408 queries for K + W <= 25, fewer beyond, >= 32
     sub = 408 if cfg["n"] > 100_000 else 1632
+    sub = max(32, min(sub, int(sub * 25 / max(W + K, 1))))
     times = []
     for k in range(W + K):
         q, y = plan[k]
