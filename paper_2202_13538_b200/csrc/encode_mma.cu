@@ -374,10 +374,16 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
 
     // ---- W^T = [W1; b1; 0]^T as a power-of-two-scaled fp16 hi + lo pair
     auto stage_wt = [&]() {
+        // each thread loads its W^T elements once (one round of loads on the
+        // critical path after the wait), takes the max, then splits them
+        constexpr int PER = (H * 16 + NT - 1) / NT;
+        float wv[PER];
         float mx = 0.f;
-        for (int i = threadIdx.x; i < (AW + 1) * H; i += NT) {
-            const float w = i < AW * H ? g.w1[i] : g.b1[i - AW * H];
-            mx = fmaxf(mx, fabsf(w));
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int i = threadIdx.x + j * NT, m = i >> 4, k = i & 15;
+            wv[j] = (i >= H * 16) ? 0.f : (k < AW ? g.w1[k * H + m] : (k == AW ? g.b1[m] : 0.f));
+            mx = fmaxf(mx, fabsf(wv[j]));
         }
 #pragma unroll
         for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
@@ -393,9 +399,11 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
         }
         __syncthreads();
         const float sc = wscale[0];
-        for (int i = threadIdx.x; i < H * 16; i += NT) {
-            const int m = i >> 4, k = i & 15;
-            const float w = (k < AW ? g.w1[k * H + m] : (k == AW ? g.b1[m] : 0.f)) * sc;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int i = threadIdx.x + j * NT, m = i >> 4, k = i & 15;
+            if (i >= H * 16) break;
+            const float w = wv[j] * sc;
             const __half hi = __float2half_rn(w);
             const __half lo = __float2half_rn(w - __half2float(hi));
             wt[m * kWS + k] = hi;
