@@ -18,6 +18,7 @@
 // The planner is a caller-owned handle holding host memory (the node ->
 // query index and the positive-tuple hash set); it touches no device state.
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
@@ -295,6 +296,15 @@ extern "C" int wj_planner_create(const int64_t *positives, int64_t n_pos, int32_
         wj::set_error("wj_planner_create: filter node id %lld out of range", (long long)filter_tuples[bad.load()]);
         return WJ_ERR_ARG;
     }
+    // WJ_PLANNER_TIMING=1: phase times of the build on stderr (profiling aid)
+    static const bool timing = getenv("WJ_PLANNER_TIMING") != nullptr;
+    auto t_start = std::chrono::steady_clock::now();
+    auto lap = [&](const char *what) {
+        if (!timing) return;
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "wj_planner_create %s: %.1f ms\n", what,
+                std::chrono::duration<double, std::milli>(now - t_start).count());
+    };
     wj_planner *p = new (std::nothrow) wj_planner();
     if (!p) {
         wj::set_error("wj_planner_create: out of host memory");
@@ -323,8 +333,10 @@ extern "C" int wj_planner_create(const int64_t *positives, int64_t n_pos, int32_
         std::vector<int64_t> fillp(p->node_off.data(), p->node_off.data() + num_nodes);
         for (int64_t q = 0; q < n_pos; ++q)
             for (int a = 0; a < arity; ++a) p->node_qids[fillp[positives[q * arity + a]]++] = q;
+        lap("validate + query index");
         if (arity <= 2) {
             p->filter1.reserve(n_filter);
+            lap("filter table allocate + clear");
             // lock-free parallel build (CAS on the 64-bit slots): the set holds
             // every positive of the split, ~30 M tuples at the citation2 shape
             // (each insert is a random DRAM access: the bucket of the tuple
@@ -343,6 +355,7 @@ extern "C" int wj_planner_create(const int64_t *positives, int64_t n_pos, int32_
             p->filter2.reserve(n_filter);
             for (int64_t i = 0; i < n_filter; ++i) p->filter2.insert(pack2(filter_tuples + i * arity, arity));
         }
+        lap("filter insert");
         p->seed_stamp.allocate(num_nodes);
         p->seed_stamp.fill(0);
         p->batch_stamp.allocate(n_pos);
