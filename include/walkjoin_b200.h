@@ -227,7 +227,10 @@ int wj_adam(float *params, float *m, float *v, const float *partial, int32_t par
             int32_t n_params, float lr, float beta1, float beta2, float eps, const int64_t *step,
             float *grad_out, float *loss_out, wj_stream_t stream);
 
-/* Step executor: one fused training step per wj_stepper_run --
+/* Step executor: one fused training step per wj_stepper_run -- replaces
+ * the body of train()'s batch loop after the batch is drawn
+ * (pipeline.py:302-305: _dense_batch -> forward -> bce_loss -> backward ->
+ * adam_step; encoder.py:126-249) --
  * wj_join_encode -> wj_encoder_tail -> wj_adam with every static argument
  * (the store's index, flat params / Adam moments at offsets9, work buffers
  * pooled [B_max, 64], s_out [B_max, A*(L+1), 64], msum [B_max, 64],
@@ -341,7 +344,8 @@ int wj_planner_next(wj_planner *planner, int64_t *queries_out, float *labels_out
  * groups_out [2n + 2] int32 = [G | start[0..G] | order[0..n)]; each tuple's
  * queries in batch order, cut into units of <= max_group members (0 = no
  * cap), larger units first (stable: first occurrence).  Host only; the
- * reference's in-seed negatives repeat tuples (~28 % of a C3 batch).  The
+ * reference's in-seed negatives (pipeline.py:132-166) repeat tuples (~28 %
+ * of a C3 batch).  The
  * producer thread of wj_planner_start_epoch uses max_group = 4. */
 int wj_group_queries(const int64_t *queries, int64_t n, int32_t arity, int32_t max_group, int32_t *groups_out,
                      int64_t *n_groups_out);
