@@ -156,3 +156,36 @@ def test_device_feeder_delivers_the_planner_batches():
     for (a, pa), (b, pb) in zip(want, got):
         assert np.array_equal(a, b) and pa == pb
     bp.close()
+
+
+def test_chain_equals_graph_hyperedges():
+    """Arity-3 queries (hyperedges, L=3): the step executor with query units
+    equals the graph step exactly."""
+    import paper_2202_13538_b200 as wj
+    from paper_2202_13538_b200 import _lib
+    from paper_2202_13538_b200.pipeline import GROUP_MAX
+
+    rng = np.random.default_rng(8)
+    g = wj.Graph.from_edges(rng.integers(0, 800, size=(9000, 2)), 800)
+    s = wj.preprocess(g, 40, 3, 4)
+    seeds = rng.choice(800, 30, replace=False)
+    batches = []
+    for B in (96, 96, 50):
+        q = np.stack([rng.choice(seeds, 3, replace=False) for _ in range(B)]).astype(np.int64)
+        gb = np.empty(5 * B + 2, np.int32)
+        _lib.call("wj_group_queries", q.ctypes.data, B, 3, GROUP_MAX, gb.ctypes.data, None)
+        y = (rng.random(B) < 0.3).astype(np.float32)
+        batches.append((torch.from_numpy(q).cuda(), torch.from_numpy(y).cuda(),
+                        (torch.from_numpy(gb).cuda(), int(gb[0]))))
+    outs = []
+    for launch in ("graph", "chain"):
+        p = wj.init_params(3, 3, dropout=0.1, seed=2)
+        st = wj.AdamState.for_params(p)
+        step = wj.TrainStep(s, p, st, use_graph=True, seed=6, launch=launch, overlap_inputs=True)
+        assert step.launch == launch
+        losses = [float(step(q, y, groups=gr)) for q, y, gr in batches]
+        torch.cuda.synchronize()
+        outs.append((losses, {k: v.clone() for k, v in p.tensors.items()}))
+    assert outs[0][0] == outs[1][0]
+    for k in outs[0][1]:
+        assert torch.equal(outs[0][1][k], outs[1][1][k]), k
