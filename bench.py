@@ -227,7 +227,7 @@ def run_ours(args, cfg):
 
     gd = []
     for q, _ in plan:
-        gb = np.empty(2 * q.shape[0] + 2, dtype=np.int32)
+        gb = np.empty((2 + q.shape[1]) * q.shape[0] + 2, dtype=np.int32)
         _lib.call("wj_group_queries", q.ctypes.data, q.shape[0], q.shape[1], GROUP_MAX, gb.ctypes.data, None)
         gd.append((torch.from_numpy(gb).to(dev), int(gb[0])))
     B_mean = float(np.mean([q.shape[0] for q, _ in plan[W:]]))

@@ -341,7 +341,8 @@ int wj_planner_get_rng(const wj_planner *planner, uint64_t *words6);
 int wj_planner_next(wj_planner *planner, int64_t *queries_out, float *labels_out, int64_t cap,
                     int64_t *n_queries_out, int64_t *n_pos_out, int64_t *n_seeds_out);
 /* Units of identical queries (same anchor tuple, same order) of a batch:
- * groups_out [2n + 2] int32 = [G | start[0..G] | order[0..n)]; each tuple's
+ * groups_out [(2 + arity) n + 2] int32 = [G | start[0..G] | order[0..n) |
+ * tuple[0..G)[arity]] (each unit's anchors; node ids < 2^31); each tuple's
  * queries in batch order, cut into units of <= max_group members (0 = no
  * cap), larger units first (stable: first occurrence).  Host only; the
  * reference's in-seed negatives (pipeline.py:132-166) repeat tuples (~28 %
@@ -354,7 +355,7 @@ int wj_group_queries(const int64_t *queries, int64_t n, int32_t arity, int32_t m
  * thread, ahead of the consumer: batches until the positives consumed reach
  * n_pos or a batch is empty, written in order into a caller-owned ring of
  * n_slots slots (ring_queries [n_slots, cap, arity], ring_labels
- * [n_slots, cap], e.g. pinned host memory; ring_groups [n_slots, 2*cap + 2]
+ * [n_slots, cap], e.g. pinned host memory; ring_groups [n_slots, (2+arity)*cap + 2]
  * or NULL receives each batch's wj_group_queries).  wj_planner_acquire spins until
  * the next batch is ready and returns its slot (-1 at the end of the epoch,
  * after which the rng state is the reference's end-of-epoch state);

@@ -350,12 +350,12 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
     int64_t *next_b = reinterpret_cast<int64_t *>(wscale + 12);
     const int32_t *gstart = g.groups ? g.groups + 1 : nullptr;
     const int32_t *gorder = g.groups ? g.groups + 2 + g.n_units : nullptr;
+    const int32_t *gtup = g.groups ? gorder + g.n_batch : nullptr;  // [G][A] each unit's anchor tuple
     auto load_meta1 = [&](int64_t uu, QMeta *dst) {  // metadata of unit uu's anchor tuple
         if (threadIdx.x < A) {
             QMeta m = {0, 0, 0, 0, 0};
             if (uu < g.n_units) {
-                const int64_t bb = gorder ? (int64_t)gorder[gstart[uu]] : uu;
-                const int64_t q = g.queries[bb * A + threadIdx.x];
+                const int64_t q = gtup ? (int64_t)gtup[uu * A + threadIdx.x] : g.queries[uu * A + threadIdx.x];
                 m.lo = g.offsets[q];
                 m.u = (int)(g.offsets[q + 1] - m.lo);
                 m.vo = g.voff[q];

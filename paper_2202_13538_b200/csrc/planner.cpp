@@ -556,7 +556,8 @@ struct GroupScratch {
     uint32_t gen = 0;
 };
 
-void emit_units(GroupScratch &sc, int64_t n, int32_t max_group, int32_t *groups_out) {
+void emit_units(GroupScratch &sc, const int64_t *queries, int32_t arity, int64_t n, int32_t max_group,
+                int32_t *groups_out) {
     // each tuple's queries in batch order, cut into units of <= max_group
     // members (the join+encode kernel runs a unit's members one after the
     // other in one CTA: a long unit would straggle), larger units first
@@ -592,6 +593,9 @@ void emit_units(GroupScratch &sc, int64_t n, int32_t max_group, int32_t *groups_
         start[r + 1] = start[r] + sc.usize[g];
         for (int32_t k = 0; k < sc.usize[g]; ++k) order[start[r] + k] = sc.members[sc.ufirst[g] + k];
     }
+    int32_t *tup = order + n;  // each unit's anchor tuple (one load for the kernel's unit metadata)
+    for (int32_t r = 0; r < G; ++r)
+        for (int a = 0; a < arity; ++a) tup[r * arity + a] = (int32_t)queries[(int64_t)order[start[r]] * arity + a];
 }
 
 }  // namespace
@@ -638,7 +642,7 @@ extern "C" int wj_group_queries(const int64_t *queries, int64_t n, int32_t arity
         sc.of[i] = sc.gid[h];
         sc.cnt[sc.gid[h]]++;
     }
-    emit_units(sc, n, max_group, groups_out);
+    emit_units(sc, queries, arity, n, max_group, groups_out);
     if (n_groups_out) *n_groups_out = groups_out[0];
     return WJ_OK;
 }
@@ -739,7 +743,7 @@ void group_planned(wj_planner *p, const int64_t *q, int64_t n, int32_t *out) {
         sc.of[i] = t;
         sc.cnt[t]++;
     }
-    emit_units(sc, n, p->group_max, out);
+    emit_units(sc, q, 2, n, p->group_max, out);
 }
 
 // The epoch loop of train() (pipeline.py:287-305): batches until the
@@ -766,7 +770,7 @@ void epoch_worker(wj_planner *p) {
             consumed += npos;
             if (rc == WJ_OK && nq > 0 && p->ring_g)
                 group_planned(p, p->ring_q + (int64_t)s * p->ring_cap * p->arity, nq,
-                              p->ring_g + (int64_t)s * (2 * p->ring_cap + 2));
+                              p->ring_g + (int64_t)s * ((2 + p->arity) * p->ring_cap + 2));
         }
         const bool last = m.n_queries < 0;
         p->slot_ready[s].store(1, std::memory_order_release);

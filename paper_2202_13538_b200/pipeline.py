@@ -272,7 +272,7 @@ class BatchPlanner:
         self._q = mk(torch.empty((self.depth, self.cap, self.arity), dtype=torch.int64))
         self._y = mk(torch.empty((self.depth, self.cap), dtype=torch.float32))
         # per slot: groups of identical queries [G | start[0..G] | order] (wj_group_queries)
-        self._g = mk(torch.empty((self.depth, 2 * self.cap + 2), dtype=torch.int32))
+        self._g = mk(torch.empty((self.depth, (2 + self.arity) * self.cap + 2), dtype=torch.int32))
         self.groups_view = None
         self._ev = [None] * self.depth
         self._i = 0
@@ -402,7 +402,7 @@ class DeviceFeeder:
     def __init__(self, planner: "BatchPlanner", device, depth: int = 4):
         self.planner, self.dev, self.depth = planner, torch.device(device), int(depth)
         self.q = torch.empty((self.depth, planner.cap, planner.arity), dtype=torch.int64, device=self.dev)
-        self.g = torch.empty((self.depth, 2 * planner.cap + 2), dtype=torch.int32, device=self.dev)
+        self.g = torch.empty((self.depth, (2 + planner.arity) * planner.cap + 2), dtype=torch.int32, device=self.dev)
         self._ng = [0] * self.depth
         self.groups, self.n_groups = None, 0  # the current batch's query groups (device) and their count
         self._ycache = {}
@@ -435,7 +435,8 @@ class DeviceFeeder:
         self._ng[s] = G
         with torch.cuda.stream(self.stream):
             self.q[s, :B].copy_(q, non_blocking=True)
-            self.g[s, :G + 2 + B].copy_(gv[:G + 2 + B], non_blocking=True)
+            self.g[s, :G + 2 + B + G * self.planner.arity].copy_(gv[:G + 2 + B + G * self.planner.arity],
+                                                                non_blocking=True)
             self.copied[s].record(self.stream)
         self.planner.release(self.copied[s])  # the pinned slot is free once copied
         return s, B, n_pos

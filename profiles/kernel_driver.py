@@ -57,7 +57,7 @@ def main():
         st = wj.AdamState.for_params(p)
         step = wj.TrainStep(store, p, st, use_graph=True, launch="chain", seed=3)
         for (q, _), qq, y in zip(plan, qd, yd):
-            gb = np.empty(2 * q.shape[0] + 2, dtype=np.int32)
+            gb = np.empty((2 + q.shape[1]) * q.shape[0] + 2, dtype=np.int32)
             _lib.call("wj_group_queries", q.ctypes.data, q.shape[0], q.shape[1], GROUP_MAX, gb.ctypes.data, None)
             step(qq, y, groups=(torch.from_numpy(gb).to(dev), int(gb[0])))
     else:

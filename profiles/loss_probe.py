@@ -20,7 +20,7 @@ qs = [torch.from_numpy(q).to(dev) for q, _ in plan]
 ys = [torch.from_numpy(y).to(dev) for _, y in plan]
 gs = []
 for q, _ in plan:
-    gb = np.empty(2 * q.shape[0] + 2, dtype=np.int32)
+    gb = np.empty((2 + q.shape[1]) * q.shape[0] + 2, dtype=np.int32)
     _lib.call("wj_group_queries", q.ctypes.data, q.shape[0], q.shape[1], GROUP_MAX, gb.ctypes.data, None)
     gs.append((torch.from_numpy(gb).to(dev), int(gb[0])))
 K = 100

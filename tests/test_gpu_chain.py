@@ -103,7 +103,7 @@ def test_chain_with_query_groups_is_bit_identical(store_and_batches):
         qq = q.numpy().copy()
         dup = rng.integers(0, qq.shape[0], size=qq.shape[0] // 2)
         qq[rng.integers(0, qq.shape[0], size=dup.shape[0])] = qq[dup]  # many repeated tuples
-        gb = np.empty(2 * qq.shape[0] + 2, np.int32)
+        gb = np.empty(4 * qq.shape[0] + 2, np.int32)
         _lib.call("wj_group_queries", qq.ctypes.data, qq.shape[0], 2, GROUP_MAX, gb.ctypes.data, None)
         assert gb[0] < qq.shape[0]
         seq.append((torch.from_numpy(qq).cuda(), y.cuda(), (torch.from_numpy(gb).cuda(), int(gb[0]))))

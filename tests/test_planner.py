@@ -144,6 +144,8 @@ def _check_groups(q, gb, cap=0):
     occurrence; every query exactly once."""
     G = int(gb[0])
     start, order = gb[1:G + 2], gb[G + 2:G + 2 + q.shape[0]]
+    tup = gb[G + 2 + q.shape[0]:G + 2 + q.shape[0] + G * q.shape[1]].reshape(G, q.shape[1])
+    assert np.array_equal(tup, q[order[start[:-1]]])  # each unit's anchor tuple
     sizes = np.diff(start)
     assert start[0] == 0 and start[-1] == q.shape[0] and np.all(sizes > 0)
     assert sorted(order.tolist()) == list(range(q.shape[0]))
@@ -183,7 +185,7 @@ def test_group_queries():
         for n in (1, 7, 500):
             q = rng.integers(0, 6, size=(n, A)).astype(np.int64)
             for cap in (0, 1, 2, 3):
-                gb = np.empty(2 * n + 2, np.int32)
+                gb = np.empty((2 + A) * n + 2, np.int32)
                 ng = ctypes.c_int64()
                 _lib.call("wj_group_queries", q.ctypes.data, n, A, cap, gb.ctypes.data, ctypes.byref(ng))
                 assert ng.value == gb[0]
