@@ -271,7 +271,7 @@ class BatchPlanner:
         self.depth = int(depth)
         self._q = mk(torch.empty((self.depth, self.cap, self.arity), dtype=torch.int64))
         self._y = mk(torch.empty((self.depth, self.cap), dtype=torch.float32))
-        # per slot: groups of identical queries [G | start[0..G] | order] (wj_group_queries)
+        # per slot: units of identical queries [G | start[0..G] | order | tuple] (wj_group_queries)
         self._g = mk(torch.empty((self.depth, (2 + self.arity) * self.cap + 2), dtype=torch.int32))
         self.groups_view = None
         self._ev = [None] * self.depth
@@ -724,7 +724,7 @@ class TrainStep:
         place (pinned host memory stays untouched until the step completes)
         and ``loss_out`` (a one-element device or pinned host tensor)
         optionally receives the loss instead; ``groups`` = (device int32
-        tensor [G | start | order] from wj_group_queries, G) lets the
+        tensor [G | start | order | tuple] from wj_group_queries, G) lets the
         join+encode kernel share the staging of identical queries."""
         B, A = q.shape
         self._prepare_bc()
