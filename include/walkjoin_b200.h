@@ -150,7 +150,12 @@ int wj_join(const int64_t *queries, int64_t n_batch, int32_t arity, const int32_
  * table_rows_f16 the fp16 table rows (wj_table_rows_f16); with them,
  * hidden = 64, A*(L+1) <= 15, L+1 <= 8 and M <= 2048 run the tensor-core
  * kernel (encode_mma.cu); otherwise (or if any of the four is NULL) the SIMT
- * kernel (wj_join_encode_simt) runs.  Replaces _kernels.join_fill +
+ * kernel (wj_join_encode_simt) runs.  keep_prob = 1 with M*(L+1) <= 1024
+ * runs the tensor-core kernel's no-dropout variant (no random stream; one
+ * row per distinct landing weighted by its row count): the same outputs, bit
+ * for bit, as every row kept.  An empty batch (n_batch = 0) only checks the
+ * shape against the kernels' envelope (WJ_ERR_UNSUPPORTED outside it).
+ * Replaces _kernels.join_fill +
  * pipeline._dense_batch + the first layer of encoder.forward/backward
  * (_kernels.py:209-245, pipeline.py:169-182, encoder.py:150-161,224-232). */
 int wj_join_encode(const int64_t *queries, int64_t n_batch, int32_t arity, const int64_t *offsets,

@@ -375,7 +375,6 @@ extern "C" int wj_join_encode_simt(const int64_t *queries, int64_t n_batch, int3
         set_error("M*(L+1) too large");
         return WJ_ERR_UNSUPPORTED;
     }
-    if (n_batch == 0) return WJ_OK;
     EncArgs g;
     g.queries = queries;
     g.n_batch = n_batch;
@@ -408,6 +407,7 @@ extern "C" int wj_join_encode_simt(const int64_t *queries, int64_t n_batch, int3
         set_error("join_encode needs %zu B of shared memory", smem);
         return WJ_ERR_UNSUPPORTED;
     }
+    if (n_batch == 0) return WJ_OK;  // an empty batch probes the envelope
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) {
         set_error("join_encode smem attribute: %s", cudaGetErrorString(e));

@@ -156,10 +156,15 @@ __device__ __forceinline__ uint32_t row_addr(uint32_t base, uint32_t l, uint32_t
 }
 
 // One tile of 16 virtual landings (list entries v0 .. v0+15) for one warp.
-// TWO = 2-row landings (Binomial(2, keep)), else 1-row (Bernoulli(keep)).
-template <bool TWO>
+// KIND 2 = 2-row landings (Binomial(2, keep)), 1 = 1-row (Bernoulli(keep)),
+// 0 = no dropout (keep = 1): the tile runs over the DISTINCT landings and G
+// is 2 n_l (n_l = the landing's row count, fp16 pairs at nl2), so the
+// statistics equal the virtual-landing sums with every row kept, exactly.
+template <int KIND>
 __device__ __forceinline__ void tile(const uint16_t *lst, uint32_t xr_s, uint32_t wt_s, int lane,
-                                     uint32_t cq, uint32_t ta, uint32_t tb, float (&sacc)[4][2][4]) {
+                                     uint32_t cq, uint32_t ta, uint32_t tb, float (&sacc)[4][2][4],
+                                     const uint32_t *nl2 = nullptr) {
+    constexpr bool TWO = KIND == 2;
     constexpr int H = 64;
     const uint32_t ib = lst[(lane & 7) + 8 * (lane >> 4)];
     const uint32_t it = lst[(lane & 7) + 8 * ((lane >> 3) & 1)];
@@ -167,6 +172,11 @@ __device__ __forceinline__ void tile(const uint16_t *lst, uint32_t xr_s, uint32_
     ldsm_x4(bx, row_addr(xr_s, ib, (lane >> 3) & 1));
     ldsm_x4_t(bt, row_addr(xr_s, it, lane >> 4));
     const uint32_t cqk = cq * 0x7feb352dU;
+    uint32_t nw[2] = {0u, 0u};
+    if (KIND == 0) {  // (2 n_l, 2 n_l') of landings 8t + 2tq, 8t + 2tq + 1
+        nw[0] = nl2[(lane & 3)];
+        nw[1] = nl2[4 + (lane & 3)];
+    }
     uint32_t ga[4][4];  // GEMM2 A fragments: G^T (unit x landing), fp16
     const int arow = (lane & 7) + 8 * ((lane >> 3) & 1), acol = 8 * (lane >> 4);
 #pragma unroll
@@ -182,6 +192,12 @@ __device__ __forceinline__ void tile(const uint16_t *lst, uint32_t xr_s, uint32_
             // z[r]: unit 16mt + gq + 8(r>>1), landing 8t + 2tq + (r&1)
 #pragma unroll
             for (int hb = 0; hb < 2; ++hb) {
+                if (KIND == 0) {
+                    const uint32_t neg =
+                        prmt(__float_as_uint(z[2 * hb]), __float_as_uint(z[2 * hb + 1]), 0xFFBBu);
+                    ga[mt][2 * t + hb] = nw[t] & ~neg;
+                    continue;
+                }
                 // hash of cq + counter (t, mt, hb): the first multiply and the
                 // counter fold into one IMAD with a compile-time addend
                 uint32_t x = cqk + ((uint32_t)t << 8 | (uint32_t)mt << 4 | (uint32_t)hb << 3) * 0x7feb352dU;
@@ -248,9 +264,10 @@ __device__ __forceinline__ void merge_cross(int tid, int nthr, int mu, const int
 
 // Row build from precomputed cross ids (wj_join_cross): no searches, the
 // fp16 table rows of kRowU landings are loaded together.
-template <int A, int W>
+template <int A, int W, bool INF>
 __device__ __forceinline__ void build_rows_x(const EncMmaArgs &g, int tid, int nthr, const int32_t *scr,
-                                             const int32_t *sid, const int (&pu)[A + 1], unsigned char *xr) {
+                                             const int32_t *sid, const int (&pu)[A + 1], unsigned char *xr,
+                                             uint16_t *vl, uint16_t *nl) {
     const int mu = g.mu;
     const int LT = pu[A];
     for (int e0 = tid; e0 < LT; e0 += kRowU * nthr) {
@@ -290,6 +307,19 @@ __device__ __forceinline__ void build_rows_x(const EncMmaArgs &g, int tid, int n
             uint32_t w[8];
             splice_row<A, W>(r, w);
             const uint32_t row = (uint32_t)rowi[u];
+            if (INF) {  // list position e -> row; 2 n_l = twice the own block's row sum (fp16)
+                const int a = (int)(row / (uint32_t)g.mu);
+                __half2 acc = __floats2half2_rn(0.f, 0.f);
+#pragma unroll
+                for (int j = 0; j < A; ++j)
+                    if (j == a)
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) acc = __hadd2(acc, *reinterpret_cast<const __half2 *>(&r[j][k]));
+                const __half n = __hadd(__low2half(acc), __high2half(acc));  // W <= 8 halves; padding is 0
+                const int e = e0 + u * nthr;
+                vl[e] = (uint16_t)row;
+                nl[e] = __half_as_ushort(__hadd(n, n));
+            }
             const uint32_t sw = (row >> 2) & 1u;
             *reinterpret_cast<uint4 *>(xr + row * kRowB + (sw << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
             *reinterpret_cast<uint4 *>(xr + row * kRowB + ((sw ^ 1u) << 4)) = make_uint4(w[4], w[5], w[6], w[7]);
@@ -297,7 +327,7 @@ __device__ __forceinline__ void build_rows_x(const EncMmaArgs &g, int tid, int n
     }
 }
 
-template <int A, int AW, int kMW, int MINB>
+template <int A, int AW, int kMW, int MINB, bool INF>
 __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaArgs g) {
     static_assert(AW + 1 <= 16, "one k16 step: A*(L+1) + 1 <= 16");
     constexpr int W = AW / A;
@@ -319,6 +349,7 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
     int32_t *sid = sx + A * mu;                                         // [A][mu] their RPE ids
     int32_t *scr = sid + A * mu;                                        // [A][A-1][mu] cross RPE ids
     uint16_t *vl = reinterpret_cast<uint16_t *>(scr + A * (A - 1) * mu);  // [lcap] virtual landing rows
+    uint16_t *nl = vl + ((A * mu + 16 + 7) & ~7);  // INF: [A*mu + 16] 2 n_l per list position (fp16)
     const uint32_t xr_s = smem_u32(xr), wt_s = smem_u32(wt);
     const uint32_t zrow = (uint32_t)(A * mu);  // all-zero row: padding (contributes nothing)
 
@@ -435,7 +466,7 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
             p2[a + 1] = p2[a] + V2[a];
             p1[a + 1] = p1[a] + V1[a];
         }
-        const int P2 = (p2[A] + 15) & ~15, P1 = (p1[A] + 15) & ~15;
+        const int P2 = INF ? 0 : (p2[A] + 15) & ~15, P1 = INF ? (pu[A] + 15) & ~15 : (p1[A] + 15) & ~15;
         // ---- stage the anchors' sorted lists (async) and the virtual-landing rows
 #pragma unroll
         for (int a = 0; a < A; ++a) {
@@ -455,7 +486,7 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
         // the anchors' virtual-landing lists (uint16, anchor-local) with the
         // anchor's row offset added: 4 loads in flight per thread
 #pragma unroll
-        for (int a = 0; a < A; ++a) {
+        for (int a = 0; a < (INF ? 0 : A); ++a) {
             const uint16_t *vs = g.vslots + qm[a].vo;
             const uint16_t add = (uint16_t)(a * mu);
             const int n2 = V2[a], nall = V2[a] + V1[a];
@@ -470,8 +501,15 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
                 }
             }
         }
-        for (int i = p2[A] + threadIdx.x; i < P2; i += NT) vl[i] = (uint16_t)zrow;
-        for (int i = P2 + p1[A] + threadIdx.x; i < P2 + P1; i += NT) vl[i] = (uint16_t)zrow;
+        if (INF) {
+            for (int i = pu[A] + threadIdx.x; i < P1; i += NT) {
+                vl[i] = (uint16_t)zrow;
+                nl[i] = 0;
+            }
+        } else {
+            for (int i = p2[A] + threadIdx.x; i < P2; i += NT) vl[i] = (uint16_t)zrow;
+            for (int i = P2 + p1[A] + threadIdx.x; i < P2 + P1; i += NT) vl[i] = (uint16_t)zrow;
+        }
         if (threadIdx.x < 2) *reinterpret_cast<uint4 *>(xr + zrow * kRowB + 16 * threadIdx.x) = make_uint4(0, 0, 0, 0);
         cp_async_wait_all();
         __syncthreads();
@@ -480,7 +518,7 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
             merge_cross<A>(threadIdx.x, NT, mu, sx, sid, U, scr);
             __syncthreads();
         }
-        build_rows_x<A, W>(g, threadIdx.x, NT, scr, sid, pu, xr);
+        build_rows_x<A, W, INF>(g, threadIdx.x, NT, scr, sid, pu, xr, vl, nl);
         __syncthreads();
 
         if (jq == 0) {
@@ -504,7 +542,7 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
         if (mem > 0) {  // the previous member's reduction overlaid the rows: rebuild them
             b = gorder[mstart + mem];
             if (threadIdx.x < 2) *reinterpret_cast<uint4 *>(xr + zrow * kRowB + 16 * threadIdx.x) = make_uint4(0, 0, 0, 0);
-            build_rows_x<A, W>(g, threadIdx.x, NT, scr, sid, pu, xr);
+            build_rows_x<A, W, INF>(g, threadIdx.x, NT, scr, sid, pu, xr, vl, nl);
             __syncthreads();
         }
         // ---- per-warp tiles of 16 virtual landings
@@ -522,10 +560,12 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
             const int v0 = tt << 4;
             // hash counter: (v0 / 2 + 4t + tq) << 6 | (16 mt + 8 hb + gq)
             const uint32_t cq = qq ^ ((uint32_t)v0 << 5) ^ ((uint32_t)tq << 6) ^ (uint32_t)gq;
-            if (tt < T2)
-                tile<true>(vl + v0, xr_s, wt_s, lane, cq, g.t21, g.t22, sacc);
+            if (INF)
+                tile<0>(vl + v0, xr_s, wt_s, lane, 0u, 0u, 0u, sacc, reinterpret_cast<const uint32_t *>(nl + v0));
+            else if (tt < T2)
+                tile<2>(vl + v0, xr_s, wt_s, lane, cq, g.t21, g.t22, sacc);
             else
-                tile<false>(vl + v0, xr_s, wt_s, lane, cq, g.t11, 0u, sacc);
+                tile<1>(vl + v0, xr_s, wt_s, lane, cq, g.t11, 0u, sacc);
         }
         __syncthreads();  // rows are dead: red overlays them
         if (dyn && mem == mcount - 1) {
@@ -658,10 +698,10 @@ __global__ void __launch_bounds__(128) join_cross_kernel(const int64_t *__restri
 
 using EncMmaKernel = void (*)(EncMmaArgs);
 
-template <int NW, int MINB>
+template <int NW, int MINB, bool INF = false>
 static EncMmaKernel pick_mma(int A, int W) {
 #define WJ_CASE(a, w) \
-    if (A == a && W == w) return join_encode_mma_kernel<a, a * w, NW, MINB>;
+    if (A == a && W == w) return join_encode_mma_kernel<a, a * w, NW, MINB, INF>;
     WJ_CASE(1, 2) WJ_CASE(1, 3) WJ_CASE(1, 4) WJ_CASE(1, 5) WJ_CASE(1, 6) WJ_CASE(1, 7) WJ_CASE(1, 8)
     WJ_CASE(2, 2) WJ_CASE(2, 3) WJ_CASE(2, 4) WJ_CASE(2, 5) WJ_CASE(2, 6) WJ_CASE(2, 7)
     WJ_CASE(3, 2) WJ_CASE(3, 3) WJ_CASE(3, 4) WJ_CASE(3, 5)
@@ -705,22 +745,29 @@ struct MmaPlan {
     size_t smem = 0;
     int slots = 0;  // resident CTAs on the device (persistent grid)
     int lcap = 0, xr_bytes = 0, mu = 1;
+    bool infer = false;
 };
 
 
-static int plan_mma(int arity, int num_walks, int num_steps, int max_unique, MmaPlan &pl) {
+// infer: the keep = 1 variant (no dropout stream; tiles over the distinct
+// landings with G = 2 n_l), usable while 2 n_l <= 2 M (L+1) is an exact
+// fp16 integer (M (L+1) <= 1024); otherwise keep = 1 runs the dropout
+// kernel with every threshold at 1.
+static int plan_mma(int arity, int num_walks, int num_steps, int max_unique, MmaPlan &pl, bool infer = false) {
     const int W = num_steps + 1;
     // CTA shape: warps x min resident CTAs per SM (register budget); tuning
     // override WJ_ENC_CFG in {"4x2", "4x3", "4x4", "8x2"}
     static const char *env_cfg = getenv("WJ_ENC_CFG");
     const int cfg = env_cfg ? (env_cfg[0] - '0') * 10 + (env_cfg[2] - '0') : 43;
     if (num_walks > 2048) return WJ_ERR_UNSUPPORTED;
-    if (cfg == 42) pl.k = pick_mma<4, 2>(arity, W);
+    const int64_t P = (int64_t)num_walks * W;
+    pl.infer = infer && P <= 1024;
+    if (pl.infer) pl.k = pick_mma<4, 3, true>(arity, W);
+    else if (cfg == 42) pl.k = pick_mma<4, 2>(arity, W);
     else if (cfg == 44) pl.k = pick_mma<4, 4>(arity, W);
     else if (cfg == 82) { pl.k = pick_mma<8, 2>(arity, W); pl.nw = 8; }
     else pl.k = pick_mma<4, 3>(arity, W);
     if (!pl.k) return WJ_ERR_UNSUPPORTED;
-    const int64_t P = (int64_t)num_walks * W;
     pl.mu = max_unique < 1 ? 1 : max_unique;
     if (P > 65535 || (int64_t)arity * pl.mu + 1 > 65535) {
         set_error("M*(L+1) or A*max_unique too large for uint16 row indices");
@@ -729,6 +776,7 @@ static int plan_mma(int arity, int num_walks, int num_steps, int max_unique, Mma
     }
     // virtual landings per query: sum_a sum_l ceil(n_l / 2) <= A (P + U) / 2, + 2 x 15 padding
     pl.lcap = (int)(((int64_t)arity * ((P + pl.mu) / 2 + 1) + 32 + 7) & ~7LL);
+    if (pl.infer) pl.lcap = 2 * ((arity * pl.mu + 16 + 7) & ~7);  // list positions + 2 n_l per position
     const int64_t rows_b = ((int64_t)arity * pl.mu + 1) * kRowB;
     const int64_t red_b = (int64_t)pl.nw * 64 * kRedS * 4;
     pl.xr_bytes = (int)(((rows_b > red_b ? rows_b : red_b) + 15) & ~15LL);
@@ -792,7 +840,8 @@ extern "C" int wj_join_encode(const int64_t *queries, int64_t n_batch, int32_t a
     }
     MmaPlan pl;
     const bool envelope = hidden == 64 && voff && vcnt && vslots && table_rows_f16;
-    int rc = envelope ? plan_mma(arity, num_walks, num_steps, max_unique, pl) : WJ_ERR_UNSUPPORTED;
+    int rc = envelope ? plan_mma(arity, num_walks, num_steps, max_unique, pl, keep_prob >= 1.f)
+                      : WJ_ERR_UNSUPPORTED;
     if (rc == WJ_ERR_CUDA) return rc;
     if (!pl.k)  // outside the tensor-core kernel's envelope (or no virtual-landing index)
         return wj_join_encode_simt(queries, n_batch, arity, offsets, uniq_x, uniq_id, num_walks, num_steps,
@@ -867,7 +916,7 @@ extern "C" int wj_stepper_create(const int64_t *offsets, const int32_t *uniq_x, 
         set_error("wj_stepper_create: out of host memory");
         return WJ_ERR_ARG;
     }
-    int rc = plan_mma(arity, num_walks, num_steps, max_unique, st->plan);
+    int rc = plan_mma(arity, num_walks, num_steps, max_unique, st->plan, keep_prob >= 1.f);
     if (rc != WJ_OK || !st->plan.k) {
         delete st;
         if (rc == WJ_OK) set_error("wj_stepper_create: shape outside the tensor-core kernel");

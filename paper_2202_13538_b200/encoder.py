@@ -181,6 +181,80 @@ def join_encode(store, q: torch.Tensor, w1: torch.Tensor, b1: torch.Tensor, keep
         _lib.call("wj_join_encode", *args, _lib.ptr(cross), *store.vindex_ptrs(), *tail)
 
 
+def fused_supported(p: ModelParams, store) -> bool:
+    """True when wj_join_encode (tensor-core or SIMT kernel) accepts this
+    model / store shape: RPE-only fp32 models whose (arity, L+1, hidden,
+    max_unique) fall inside an instantiated kernel.  Probed once per (store,
+    arity, hidden) with an empty batch, which runs the library's own envelope
+    checks; callers route other shapes to dense_batch + ``forward``."""
+    if p.feature_dim or p.w1.dtype != torch.float32:
+        return False
+    cache = store.__dict__.setdefault("_fused_ok", {})
+    key = (p.arity, p.hidden)
+    if key not in cache:
+        if store.voff_d is None:
+            store.build_vindex()
+        t = p.tensors
+        q = torch.empty((0, p.arity), dtype=torch.int64, device=store.device)
+        pooled = torch.empty((1, p.hidden), dtype=torch.float32, device=store.device)
+        try:
+            join_encode(store, q, t["w1"], t["b1"], 1.0, 0, None, pooled)
+            cache[key] = True
+        except NotImplementedError:
+            cache[key] = False
+    return cache[key]
+
+
+TAIL_AW = (2, 3, 4, 5, 6, 7, 8, 9, 10, 12, 14, 15, 16)  # A*(L+1) instantiated by wj_encoder_tail
+
+
+class FusedScorer:
+    """Scoring without dropout or gradients, two kernels per chunk:
+    wj_join_encode at keep = 1 (its no-dropout variant: distinct landings
+    weighted by their row counts, no random stream, no S / msum output) ->
+    wj_encoder_tail in logits mode (W2 layer, classifier).  Replaces
+    pipeline._score_array's _dense_batch -> forward(training=False)
+    (pipeline.py:185-198, encoder.py:126-180).  Needs hidden = 64 and an
+    instantiated A*(L+1); the parameters are copied into one flat buffer at
+    construction (call ``refresh()`` after they change)."""
+
+    def __init__(self, p: ModelParams, store):
+        import ctypes
+
+        if not (fused_supported(p, store) and p.hidden == 64 and p.arity * store.width in TAIL_AW):
+            raise NotImplementedError("fused scoring needs an RPE-only fp32 model with hidden = 64")
+        self.p, self.store = p, store
+        sizes = [p.tensors[k].numel() for k in TENSOR_ORDER]
+        self.offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
+        self.offs_c = (ctypes.c_int32 * 9)(*[int(x) for x in self.offs])
+        self.flat = torch.empty(int(self.offs[-1]), dtype=torch.float32, device=store.device)
+        self.refresh()
+        self._bufs = {}
+
+    def refresh(self) -> None:
+        torch.cat([self.p.tensors[k].reshape(-1).to(torch.float32) for k in TENSOR_ORDER], out=self.flat)
+
+    def logits(self, q: torch.Tensor) -> torch.Tensor:
+        """q [B, A] int64 on the store's device (ids already validated)."""
+        from . import _lib
+
+        B, A = q.shape
+        dev = self.store.device
+        buf = self._bufs.get(B)
+        if buf is None:
+            buf = (torch.empty((B, 64), dtype=torch.float32, device=dev),
+                   torch.empty(B, dtype=torch.float32, device=dev))
+            self._bufs = {B: buf}
+        pooled, logits = buf
+        t = self.p.tensors
+        join_encode(self.store, q, t["w1"], t["b1"], 1.0, 0, None, pooled)
+        scale = 1.0 / (A * self.store.landings)
+        _lib.call("wj_encoder_tail", _lib.ptr(pooled), None, None, None, B, A * self.store.width, 64,
+                  _lib.ptr(self.flat), self.offs_c, scale, _lib.ptr(logits), None, 0, None, None,
+                  _lib.stream_handle(dev))
+        return logits
+
+
 def forward_fused(p: ModelParams, store, q: torch.Tensor, training: bool = False, seed: int = 0,
                   step: Optional[torch.Tensor] = None, need_grad: bool = True, out: dict = None,
                   tail: bool = True):
@@ -313,8 +387,9 @@ def adam_step(p: ModelParams, grads: dict, state: AdamState) -> None:
 
 def adam_step_graphable(p: ModelParams, grads: dict, state: AdamState, inv_bc: torch.Tensor) -> None:
     """Adam with the bias corrections read from a device tensor
-    ``inv_bc = [1/(1-beta1^t), 1/(1-beta2^t)]`` that the host refreshes before
-    each replay, so the update can live inside a captured CUDA graph."""
+    ``inv_bc = [1/(1-beta1^t), 1/(1-beta2^t)]`` (TrainStep derives it on the
+    device from its step counter), so the update can live inside a captured
+    CUDA graph."""
     for name in TENSOR_ORDER:
         g = grads[name]
         tensor = p.tensors[name]

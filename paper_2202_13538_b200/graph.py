@@ -123,8 +123,10 @@ def _parse_int(tok: str, lineno: int) -> int:
     return v
 
 
-def load_edge_list(lines: Iterable[str]) -> Graph:
-    """``u v`` per line, '#' comments, dense remap by first appearance (graph.py:149-179)."""
+def load_edge_list(lines: Iterable[str], undirected: bool = True) -> Graph:
+    """``u v`` per line, '#' comments, dense remap by first appearance
+    (graph.py:149-179).  ``undirected=False``: the input must already list
+    both directions of every edge (validated, GraphFormatError otherwise)."""
     id_map: dict = {}
     pairs = []
     for lineno, raw in enumerate(lines, 1):
@@ -141,7 +143,13 @@ def load_edge_list(lines: Iterable[str]) -> Graph:
         pairs.append((id_map[u], id_map[v]))
     if not id_map:
         raise GraphFormatError("empty edge list")
-    return Graph.from_edges(np.array(pairs, np.int64), len(id_map), id_map=id_map)
+    arr = np.array(pairs, np.int64)
+    if not undirected:
+        fwd = set(map(tuple, arr.tolist()))
+        missing = [e for e in fwd if (e[1], e[0]) not in fwd and e[0] != e[1]]
+        if missing:
+            raise GraphFormatError(f"directed input is not symmetric, e.g. edge {missing[0]}")
+    return Graph.from_edges(arr, len(id_map), id_map=id_map)
 
 
 def project_hyperedges(lines: Iterable[str]) -> Graph:

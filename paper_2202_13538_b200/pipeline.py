@@ -23,6 +23,7 @@ import torch
 
 from . import _lib
 from . import encoder as E
+from .graph import Query
 from .joiner import dense_batch
 from .store import SubgraphStore
 
@@ -88,13 +89,13 @@ def canonical_nodes(nodes) -> tuple:
 
 
 def sample_minibatch(index: QueryOverlapIndex, queries, cfg: TrainConfig, rng: np.random.Generator,
-                     n_seeds: Optional[int] = None, exact: bool = False):
+                     n_seeds: Optional[int] = None, exact: bool = True):
     """BFS over query-sharing neighbours (pipeline.py:77-129).
 
-    ``exact=True`` draws the seed nodes with ``rng.choice(..., replace=False)``
-    exactly like the reference (a full permutation of the node list per
-    batch); the default draws the same uniform distinct subset by rejection,
-    which is O(n_seeds)."""
+    ``exact=True`` (the default, the reference's draw) takes the seed nodes
+    with ``rng.choice(..., replace=False)`` exactly like the reference (a
+    full permutation of the node list per batch); ``exact=False`` draws the
+    same uniform distinct subset by rejection, which is O(n_seeds)."""
     if len(index) == 0:
         raise ValueError("empty training query set")
     if n_seeds is None:
@@ -164,13 +165,14 @@ class PositiveFilter:
         return self.keys[pos] == k if len(self.keys) else np.zeros(len(k), bool)
 
 
-def sample_negatives(seed_set: Sequence[int], arity: int, count: int, positive_filter,
-                     rng: np.random.Generator) -> np.ndarray:
+def sample_negatives_array(seed_set: Sequence[int], arity: int, count: int, positive_filter,
+                           rng: np.random.Generator) -> np.ndarray:
     """Uniform distinct-node tuples inside the seed set, rejected against the
-    positives (pipeline.py:132-166).  Vectorised per chunk with the same rng
-    draws and acceptance order as the reference loop, so for the same
-    generator state it returns the same queries.  ``positive_filter`` is a
-    PositiveFilter or a set of canonical tuples."""
+    positives (pipeline.py:132-166), as an int64 [count, arity] array.
+    Vectorised per chunk with the same rng draws and acceptance order as the
+    reference loop, so for the same generator state it returns the same
+    queries.  ``positive_filter`` is a PositiveFilter or a set of canonical
+    tuples."""
     nodes = np.asarray(list(seed_set), dtype=np.int64)
     if nodes.shape[0] < arity:
         raise ValueError(f"seed set of {nodes.shape[0]} nodes cannot host arity-{arity} negatives")
@@ -198,11 +200,19 @@ def sample_negatives(seed_set: Sequence[int], arity: int, count: int, positive_f
     return np.concatenate(out) if out else np.empty((0, arity), np.int64)
 
 
+def sample_negatives(seed_set: Sequence[int], arity: int, count: int, positive_filter,
+                     rng: np.random.Generator) -> list:
+    """The reference signature and return type (pipeline.py:132-166): a list
+    of label-0 ``Query`` objects, same draws as ``sample_negatives_array``."""
+    arr = sample_negatives_array(seed_set, arity, count, positive_filter, rng)
+    return [Query(tuple(int(v) for v in row), 0) for row in arr.tolist()]
+
+
 def make_batch(index, positives: np.ndarray, pos_filter, cfg: TrainConfig, rng, exact=False):
     """One batch of query ids + labels (pipeline.py:293-304)."""
     seeds, ids = sample_minibatch(index, positives, cfg, rng, exact=exact)
     pos = positives[np.asarray(ids, dtype=np.int64)]
-    negs = sample_negatives(seeds, positives.shape[1], cfg.k_neg * len(ids), pos_filter, rng)
+    negs = sample_negatives_array(seeds, positives.shape[1], cfg.k_neg * len(ids), pos_filter, rng)
     q = np.concatenate([pos, negs]).astype(np.int64)
     labels = np.concatenate([np.ones(len(ids)), np.zeros(len(negs))]).astype(np.float32)
     return q, labels
@@ -492,15 +502,17 @@ class TrainStep:
                  features: Optional[torch.Tensor] = None, overlap_inputs: bool = False, launch: str = "graph"):
         if features is not None and mode == "fused":
             raise ValueError("node features need mode='pooled' or 'reference' (the fused kernel is RPE-only)")
+        if mode == "fused" and not E.fused_supported(params, store):
+            # outside every fused kernel's envelope: the dense join + PyTorch encoder
+            mode = "pooled"
         self.store, self.params, self.state = store, params, state
         self.features = features
         self.dense_dtype, self.mode, self.use_graph = dense_dtype, mode, use_graph
         self.group = process_group
         self.seed = int(seed)
         self.dev = store.device
-        self.inv_bc = torch.ones(2, dtype=params.w1.dtype, device=self.dev)
-        self._host_bc = torch.ones(2, dtype=params.w1.dtype).pin_memory()
-        self.step_t = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        self.inv_bc = None
+        self.step_t = torch.full((1,), int(state.step), dtype=torch.int64, device=self.dev)
         self._graphs: dict = {}
         self._slot: dict = {}
         self._copy_stream = torch.cuda.Stream(self.dev) if use_graph else None
@@ -508,7 +520,7 @@ class TrainStep:
         # fused + hidden 64: tail and Adam as two CUDA kernels on flat buffers
         self.fast_tail = (mode == "fused" and params.hidden == 64 and params.feature_dim == 0
                           and params.w1.dtype == torch.float32
-                          and store.width * params.arity in (2, 3, 4, 5, 6, 8, 9, 10, 12, 14, 15, 16))
+                          and store.width * params.arity in (2, 3, 4, 5, 6, 7, 8, 9, 10, 12, 14, 15, 16))
         if fast_tail is not None:
             self.fast_tail = self.fast_tail and fast_tail
         if self.fast_tail:
@@ -539,6 +551,14 @@ class TrainStep:
         self._loss_hist = None
         self._n_calls = 0
         self.input_event = None
+        if self.launch == "chain":
+            # the step executor needs the tensor-core kernel and the store's
+            # virtual-landing index; other shapes step through the graph path
+            try:
+                self._make_stepper(16)
+            except (NotImplementedError, ValueError):
+                self._stepper, self._stepper_cap = None, 0
+                self.launch = "graph"
 
     def _buffers(self, B, A):
         if self.mode == "fused":
@@ -602,17 +622,18 @@ class TrainStep:
             from .distributed import all_reduce_grads
 
             all_reduce_grads(grads, E.TENSOR_ORDER, self.group)
+        # Adam bias corrections from the device step counter (already advanced
+        # for this step), so they stay in stream order with the step itself
+        t = self.step_t.to(self.params.w1.dtype)
+        st = self.state
+        inv_bc = 1.0 / (1.0 - torch.cat([torch.pow(st.beta1, t), torch.pow(st.beta2, t)]))
         E.adam_step_graphable(self.params, grads, self.state, inv_bc)
         return loss
 
     def _prepare_bc(self):
+        # host bookkeeping only: every path derives Adam's bias corrections
+        # on the device from the step counter
         self.state.step += 1
-        if self.fast_tail:  # the kernel path derives the corrections from the device step counter
-            return
-        t = self.state.step
-        self._host_bc[0] = 1.0 / (1.0 - self.state.beta1 ** t)
-        self._host_bc[1] = 1.0 / (1.0 - self.state.beta2 ** t)
-        self.inv_bc.copy_(self._host_bc, non_blocking=True)
 
     # ------------------------------------------------------------ chain mode
     _LOSS_HIST = 4096
@@ -821,19 +842,36 @@ def _rows(queries) -> np.ndarray:
     return np.asarray([getattr(q, "nodes", q) for q in queries], dtype=np.int64)
 
 
+def _check_ids(store: SubgraphStore, q: torch.Tensor) -> None:
+    """One range check of a device query batch (joiner.py:40-50)."""
+    if q.numel() and (int(q.min()) < 0 or int(q.max()) >= store.num_nodes):
+        raise ValueError(f"query node ids must lie in [0, {store.num_nodes})")
+
+
 def score_array(store: SubgraphStore, params: E.ModelParams, query_array, features=None,
-                chunk: int = 8192) -> torch.Tensor:
+                chunk: int = 8192, validate: bool = True) -> torch.Tensor:
     """Sigmoid scores of a query array as a float64 DEVICE tensor
     (pipeline.py:185-198 without the host round trip).  RPE-only fp32 models
-    score through the fused join+encode kernel; feature models through the
-    dense join kernel + PyTorch encoder."""
+    inside the fused kernels' envelope score through wj_join_encode (keep = 1:
+    no dropout stream, no backward statistics); feature models and other
+    shapes through the dense join kernel + PyTorch encoder."""
     q_all = torch.as_tensor(query_array, dtype=torch.int64).to(store.device)
     if q_all.shape[0] == 0:
         return torch.empty(0, dtype=torch.float64, device=store.device)
+    if q_all.dim() != 2 or q_all.shape[1] != params.arity:
+        raise ValueError(f"queries must be [B, {params.arity}] for this model")
+    if validate:
+        _check_ids(store, q_all)
+    fused = features is None and E.fused_supported(params, store)
+    scorer = None
+    if fused and params.hidden == 64 and params.arity * store.width in E.TAIL_AW:
+        scorer = E.FusedScorer(params, store)  # join+encode (keep = 1) -> tail kernel
     out = []
     for lo in range(0, q_all.shape[0], chunk):
         q = q_all[lo: lo + chunk]
-        if features is None and params.feature_dim == 0 and params.w1.dtype == torch.float32:
+        if scorer is not None:
+            logits = scorer.logits(q).clone()
+        elif fused:
             logits, _ = E.forward_fused(params, store, q, training=False, need_grad=False)
         else:
             dense = dense_batch(store, q, features=features, dtype=params.w1.dtype, validate=False)
@@ -943,7 +981,7 @@ def train(store: SubgraphStore, split, cfg: TrainConfig, features=None, train_ne
             if pool is not None:
                 negs = pool[batch_rng.integers(0, pool.shape[0], size=n_neg)]
             else:
-                negs = sample_negatives(seeds, arity, n_neg, pos_filter, batch_rng)
+                negs = sample_negatives_array(seeds, arity, n_neg, pos_filter, batch_rng)
             q = torch.from_numpy(np.concatenate([pos, negs]).astype(np.int64))
             y = torch.from_numpy(np.concatenate([np.ones(len(ids)), np.zeros(negs.shape[0])]).astype(np.float32))
             loss_sum += step(q, y).double()
@@ -964,22 +1002,36 @@ def train(store: SubgraphStore, split, cfg: TrainConfig, features=None, train_ne
 
 
 def infer(store: SubgraphStore, params: E.ModelParams, queries, threads: int = 1, features=None,
-          chunk: int = 2048) -> np.ndarray:
-    """Sigmoid scores, input order (pipeline.py:329-355)."""
+          chunk: int = 8192) -> np.ndarray:
+    """Sigmoid scores, input order (pipeline.py:329-355): the reference's
+    checks (arity, feature_dim / feature matrix), one range check of every
+    query id, then ``score_array``."""
     if len(queries) == 0:
         return np.empty(0, dtype=np.float64)
-    rows = np.asarray([getattr(q, "nodes", q) for q in queries], dtype=np.int64)
+    if isinstance(queries, np.ndarray):
+        rows = queries.astype(np.int64, copy=False)
+        if rows.ndim != 2:
+            raise ValueError("queries must share one arity")
+    else:
+        lists = [tuple(getattr(q, "nodes", q)) for q in queries]
+        if len(lists[0]) != params.arity:
+            raise ValueError(f"queries have arity {len(lists[0])} but model was trained with arity {params.arity}")
+        if any(len(r) != params.arity for r in lists):
+            raise ValueError("queries must share one arity")
+        rows = np.asarray(lists, dtype=np.int64)
     if rows.shape[1] != params.arity:
         raise ValueError(f"queries have arity {rows.shape[1]} but model was trained with arity {params.arity}")
-    out = []
-    q_all = torch.from_numpy(rows).to(store.device)
-    for lo in range(0, rows.shape[0], chunk):
-        if features is None and params.feature_dim == 0 and params.w1.dtype == torch.float32:
-            logits, _ = E.forward_fused(params, store, q_all[lo: lo + chunk], training=False,
-                                        need_grad=False)
-        else:
-            dense = dense_batch(store, q_all[lo: lo + chunk], features=features,
-                                dtype=params.w1.dtype)
-            logits, _ = E.forward(params, dense, training=False)
-        out.append(torch.sigmoid(logits.double()))
-    return torch.cat(out).cpu().numpy()
+    if params.feature_dim > 0:
+        if features is None:
+            raise ValueError("model expects node features but none were given")
+        f = features if isinstance(features, torch.Tensor) else np.asarray(features, dtype=np.float64)
+        if f.shape[0] != store.num_nodes:
+            raise ValueError(f"feature matrix has {f.shape[0]} rows for {store.num_nodes} nodes")
+        if f.shape[1] != params.feature_dim:
+            raise ValueError(f"feature matrix width {f.shape[1]} != model feature_dim {params.feature_dim}")
+        features = torch.as_tensor(f, dtype=params.w1.dtype, device=store.device)
+    else:
+        features = None  # the reference ignores features for an RPE-only model
+    if rows.size and (rows.min() < 0 or rows.max() >= store.num_nodes):
+        raise ValueError(f"query node ids must lie in [0, {store.num_nodes})")
+    return score_array(store, params, rows, features=features, chunk=chunk, validate=False).cpu().numpy()

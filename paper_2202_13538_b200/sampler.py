@@ -107,10 +107,12 @@ def _next_pow2(v: int) -> int:
     return 1 << max(1, (int(v) - 1).bit_length())
 
 
-def intern_device(uniq_key, uniq_first, offsets, n_anchors, anchor_base, num_walks, width):
+def intern_device(uniq_key, uniq_first, offsets, n_anchors, anchor_base, num_walks, width, return_order=False):
     """Global RPE ids for every entry: phase 1/3 on device, phase 2 (order the
     distinct vectors by first occurrence) with torch.  Returns
-    (uniq_id int32 [E], table_keys int64 [T] with row 0 = 0)."""
+    (uniq_id int32 [E], table_keys int64 [T] with row 0 = 0) [+ the scan
+    order (anchor << 16 | first) of each id's first occurrence, int64 [T-1],
+    with ``return_order``]."""
     dev = uniq_key.device
     total = int(uniq_key.numel())
     s = _lib.stream_handle(dev)
@@ -134,6 +136,8 @@ def intern_device(uniq_key, uniq_first, offsets, n_anchors, anchor_base, num_wal
     uniq_id = torch.empty(total, dtype=torch.int32, device=dev)
     _lib.call("wj_intern_assign", _lib.ptr(uniq_key), total, _lib.ptr(keys), _lib.ptr(ids), cap,
               _lib.ptr(uniq_id), s)
+    if return_order:
+        return uniq_id, table_keys, order[occ[perm]]
     return uniq_id, table_keys
 
 

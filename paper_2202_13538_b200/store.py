@@ -282,6 +282,97 @@ def get_rpe_id(store: SubgraphStore, u: int, x: int) -> int:
     return int(out.item())
 
 
+def _default_device():
+    if not torch.cuda.is_available():
+        raise RuntimeError("walkjoin_b200 needs a CUDA device (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def intern_vectors_device(vecs: torch.Tensor):
+    """Global interning of [R, W] int32 count vectors on the device
+    (store.py:107-121, _kernels.py:137-171): ids 1-based in first-occurrence
+    order of the rows, table [T, W] with the zero row prepended.  Returns
+    device tensors (ids int32 [R], table int32 [T, W], reps int64 [T-1] =
+    first row of each id).
+
+    Rows whose counts pack into 63 bits (every store's vectors: W fields of
+    bit_length(max) bits) go through the preprocess interning kernels
+    (wj_intern_insert / wj_intern_assign), each row its own scan position;
+    any other int32 rows (negative or very wide) are ranked with a device
+    ``unique`` -- the same definition, first occurrence -> id."""
+    from .sampler import intern_device
+
+    vecs = vecs.to(torch.int32).contiguous()
+    R, W = vecs.shape
+    dev = vecs.device
+    if R == 0:
+        return (torch.empty(0, dtype=torch.int32, device=dev), torch.zeros((1, W), dtype=torch.int32, device=dev),
+                torch.empty(0, dtype=torch.int64, device=dev))
+    vmin, vmax = int(vecs.min()), int(vecs.max())
+    cb = max(1, vmax.bit_length())
+    if vmin >= 0 and W * cb <= 63 and R < (1 << 46):
+        shifts = torch.arange(W, device=dev, dtype=torch.int64) * cb
+        # the marker bit keeps an all-zero row distinct from the empty slot
+        key = ((vecs.to(torch.int64) << shifts[None, :]).sum(1)) | (1 << 63)
+        offsets = torch.arange(R + 1, dtype=torch.int64, device=dev)
+        first = torch.zeros(R, dtype=torch.int16, device=dev)
+        ids, keys_sorted, orders = intern_device(key, first, offsets, R, 0, None, W, return_order=True)
+        reps = orders >> 16
+    else:
+        uniq, inv = torch.unique(vecs, dim=0, return_inverse=True)
+        rows = torch.arange(R, dtype=torch.int64, device=dev)
+        first = torch.full((uniq.shape[0],), R, dtype=torch.int64, device=dev)
+        first.scatter_reduce_(0, inv, rows, reduce="amin")
+        order = torch.argsort(first)
+        rank = torch.empty_like(order)
+        rank[order] = torch.arange(order.numel(), device=dev)
+        ids = (rank[inv] + 1).to(torch.int32)
+        reps = first[order]
+    table = torch.zeros((reps.numel() + 1, W), dtype=torch.int32, device=dev)
+    table[1:] = vecs[reps]
+    return ids, table, reps
+
+
+def intern_vectors(vecs) -> tuple:
+    """store.py:107-121 on the device: (ids int32 1-based, table int32 with
+    the zero row), host numpy in -> host numpy out like the reference."""
+    on_host = not isinstance(vecs, torch.Tensor) or vecs.device.type == "cpu"
+    v = torch.as_tensor(np.ascontiguousarray(vecs, dtype=np.int32) if not isinstance(vecs, torch.Tensor) else vecs)
+    if v.dim() != 2:
+        raise ValueError("intern_vectors expects a [rows, width] array")
+    if v.device.type == "cpu":
+        v = v.to(_default_device())
+    ids, table, _ = intern_vectors_device(v)
+    if on_host:
+        return ids.cpu().numpy(), table.cpu().numpy()
+    return ids, table
+
+
+def dedup_and_reindex(raw_maps: Sequence):
+    """store.py:134-157: the deduplicated table and per-node {x: id} dicts
+    from raw per-node positional count maps (ascending node order, entries in
+    their recorded first-appearance order); the interning runs on the
+    device (``intern_vectors``)."""
+    vec_rows, node_lists, width = [], [], None
+    for raw in raw_maps:
+        entries = raw.entries if hasattr(raw, "entries") else raw
+        nodes = list(entries.keys())
+        node_lists.append(nodes)
+        for x in nodes:
+            vec = np.asarray(entries[x], dtype=np.int32)
+            if width is None:
+                width = vec.shape[0]
+            vec_rows.append(vec)
+    if width is None:
+        raise ValueError("no raw maps given")
+    ids, table = intern_vectors(np.array(vec_rows, dtype=np.int32))
+    dicts, pos = [], 0
+    for nodes in node_lists:
+        dicts.append({int(x): int(ids[pos + i]) for i, x in enumerate(nodes)})
+        pos += len(nodes)
+    return RpeTable(table), dicts
+
+
 def get_rpe_ids(store: SubgraphStore, u: torch.Tensor, x: torch.Tensor) -> torch.Tensor:
     """Batched device lookups (no range check on u beyond the caller's)."""
     u = u.to(store.device, torch.int64).contiguous()

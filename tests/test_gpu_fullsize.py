@@ -109,6 +109,26 @@ def test_c3_sampled_anchors_bit_exact_vs_oracle(c3):
             np.testing.assert_array_equal(tab[ri[b][:, a]], want)
 
 
+def test_c3_interning_order_every_id(c3):
+    """At the headline size: every global RPE id is the first-occurrence
+    rank of its vector in (anchor, first appearance) order, and each table
+    row is the count vector of that first entry recomputed from the walks
+    (the sequential definition _kernels.py:137-171)."""
+    from test_gpu_configs import interning_order_check
+
+    g, s = c3
+    interning_order_check(s)
+
+
+def test_c3_sampled_first_appearance_slots(c3):
+    from test_gpu_configs import sampled_anchors_vs_oracle
+
+    g, s = c3
+    rng = np.random.default_rng(17)
+    nodes = np.unique(rng.integers(0, g.num_nodes, 64))
+    sampled_anchors_vs_oracle(g, s, nodes, 3)
+
+
 def test_c3_fused_encoder_vs_dense_reference(c3):
     """The fused join+encode kernel at the headline size (lists of ~530
     distinct landings per anchor, the training batch's query mix) against the

@@ -54,9 +54,21 @@ def test_minibatcher_and_negatives_reproduce_reference(golden_meta):
         seeds, ids = sample_minibatch(index, pos, cfg, rng, exact=True)
         negs = sample_negatives(seeds, 2, cfg.k_neg * len(ids), filt, rng)
         assert seeds == want["seeds"] and ids == want["ids"]
-        assert negs.tolist() == want["negs"]
+        assert [list(q.nodes) for q in negs] == want["negs"] and all(q.label == 0 for q in negs)
+    # the package-level exports are the reference's names and defaults: the
+    # same generator gives the same batches through them, with a set filter
+    import paper_2202_13538_b200 as wj
+
+    rng = np.random.default_rng(mb["rng_seed"])
+    index2 = wj.QueryOverlapIndex([wj.Query(tuple(r), 1) for r in pos.tolist()])
+    sfilt = {tuple(sorted(r)) for r in allpos.tolist()}
+    for want in mb["batches"]:
+        seeds, ids = wj.sample_minibatch(index2, pos, cfg, rng)
+        negs = wj.sample_negatives(seeds, 2, cfg.k_neg * len(ids), sfilt, rng)
+        assert seeds == want["seeds"] and ids == want["ids"]
+        assert [list(q.nodes) for q in negs] == want["negs"]
     # the fast seed draw gives a valid batch of the same shape contract
-    seeds, ids = sample_minibatch(index, pos, cfg, np.random.default_rng(0))
+    seeds, ids = sample_minibatch(index, pos, cfg, np.random.default_rng(0), exact=False)
     assert 0 < len(ids) <= cfg.batch_size and len(seeds) <= cfg.batch_capacity
     assert all(any(v in set(seeds) for v in pos[i]) for i in ids)
 
