@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "_walkjoin_b200.so")
-SOURCES = ["capi.cu", "sampler.cu", "rpe.cu", "intern.cu", "join.cu", "encode.cu", "encode_mma.cu", "tail.cu",
+SOURCES = ["capi.cu", "sampler.cu", "rpe.cu", "intern.cu", "join.cu", "encode.cu", "encode_mma.cu", "encode_tc.cu", "tail.cu",
            "vindex.cu", "surl.cu", "planner.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

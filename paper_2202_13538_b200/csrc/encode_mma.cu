@@ -34,60 +34,13 @@
 //    z = [x | 1] W1aug, so pooled[h] = sum_c W1aug[c][h] S^T[h][c].
 //
 // One CTA (8 warps) per query, persistent; each warp owns every 8th tile.
-#include <cuda_fp16.h>
-
+#include <cstdio>
 #include <cstdlib>
 #include <new>
 
-#include "common.cuh"
+#include "encode_common.cuh"
 
 namespace wj {
-
-constexpr int kWS = 24;       // halves per staged W^T row (48 B: conflict-free ldmatrix)
-constexpr int kRedS = 17;     // floats per unit in the reduction buffer (16 S^T cols + pad)
-constexpr int kRowB = 32;     // bytes per landing row [x | 1 | 0..] (16 halves)
-constexpr int kWtBytes = 2 * 64 * kWS * 2;
-constexpr int kRowU = 4;      // landings per thread per batch in the row build
-constexpr int kMetaQ = 16;    // queries whose metadata a CTA loads at once
-struct QMeta {
-    int64_t lo, vo;  // first entry of the anchor's sorted list / of its virtual landings
-    int u, v2, v1;   // list length, 2-row and 1-row virtual landings
-};
-constexpr int kHdrBytes = (kMetaQ * 3 * (int)sizeof(QMeta) + 16 + 32 + 16 + 15) & ~15;  // meta | wscale[4] | wred[8] | next_b
-
-struct EncMmaArgs {
-    const int64_t *queries;
-    int64_t n_batch;
-    const int64_t *offsets;
-    const int32_t *ux;
-    const int32_t *uid;
-    const int64_t *voff;
-    const int32_t *vcnt;
-    const uint16_t *vslots;
-    const uint4 *trow;  // [tlen] fp16 count rows (8 halves)
-    int mu, lcap, xr_bytes;
-    const int32_t *cross;  // [B][A][A-1][mu] cross RPE ids (wj_join_cross) or null: search in-kernel
-    const float *w1;  // [AW, 64]
-    const float *b1;  // [64]
-    uint32_t t11, t21, t22;  // packed 14-bit thresholds (both lanes): 1-row; 2-row K>=1, K>=2
-    uint64_t seed;
-    const int64_t *step;
-    float *pooled;  // [B, 64]
-    float *s_out;   // [B, AW, 64] or null
-    float *msum;    // [B, 64] or null
-    int32_t *qsched;  // [2] zeroed query-grab / done counters (dynamic scheduling) or null: static striding
-    // dynamic scheduling over groups of identical queries (null: one query
-    // per unit): [G | start[0..G] | order[0..B)] -- unit u = the queries
-    // order[start[u] .. start[u+1]), all with the same anchor tuple, so the
-    // unit stages, merges and builds its rows once and runs tiles +
-    // reduction per member (each with its own dropout stream and outputs)
-    const int32_t *groups;
-    int64_t n_units;  // G with groups, else n_batch
-};
-
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
 
 __device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
@@ -109,51 +62,6 @@ __device__ __forceinline__ void hmma(float (&d)[4], const uint32_t (&a)[4], uint
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-// byte permute with the sign-replicate mode (selector nibble bit 3)
-__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
-    uint32_t r;
-    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
-    return r;
-}
-
-__device__ __forceinline__ uint32_t hadd2_u32(uint32_t a, uint32_t b) {
-    uint32_t r;
-    asm("add.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
-    return r;
-}
-
-// Output word k of the row [x | 1 | 0...] (16 fp16 columns), where column
-// c < A*W is count f = c % W of anchor block j = c / W, taken from the fp16
-// table row r[j] (W <= 8 halves in 4 words), column A*W is 1.0.  All
-// selectors are compile-time constants after unrolling: one PRMT per word.
-template <int A, int W>
-__device__ __forceinline__ uint32_t half_src(const uint32_t (&r)[A][4], int c, int &sel_hi) {
-    constexpr int AW = A * W;
-    if (c < AW) {
-        const int j = c / W, f = c % W;
-        sel_hi = f & 1;
-        return r[j][f >> 1];
-    }
-    sel_hi = 0;
-    return c == AW ? 0x3C003C00u : 0u;
-}
-
-template <int A, int W>
-__device__ __forceinline__ void splice_row(const uint32_t (&r)[A][4], uint32_t (&out)[8]) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        int h0, h1;
-        const uint32_t x = half_src<A, W>(r, 2 * k, h0);
-        const uint32_t y = half_src<A, W>(r, 2 * k + 1, h1);
-        out[k] = __byte_perm(x, y, (h0 ? 0x32u : 0x10u) | ((h1 ? 0x76u : 0x54u) << 8));
-    }
-}
-
-// row l's two 16-B halves are XOR-swizzled by bit 2 of l, so the 8 rows of
-// an ldmatrix phase are bank-conflict-free when they are consecutive
-__device__ __forceinline__ uint32_t row_addr(uint32_t base, uint32_t l, uint32_t half) {
-    return base + l * kRowB + (((half ^ (l >> 2)) & 1u) << 4);
-}
 
 // One tile of 16 virtual landings (list entries v0 .. v0+15) for one warp.
 // KIND 2 = 2-row landings (Binomial(2, keep)), 1 = 1-row (Bernoulli(keep)),
@@ -220,113 +128,6 @@ __device__ __forceinline__ void tile(const uint16_t *lst, uint32_t xr_s, uint32_
     }
 }
 
-// Cross RPE ids by merging the anchors' sorted lists (merge path): for every
-// anchor pair (a, j) thread tid of nthr takes an equal slice of the merged
-// order (one diagonal binary search, then a linear merge); equal ids are
-// emitted list-a first, so an element of list j finds its partner at list a's
-// previous position.  scr[a][jj][l] = RPE id of landing l of anchor a relative
-// to the jj-th other anchor (0 if absent).
-template <int A>
-__device__ __forceinline__ void merge_cross(int tid, int nthr, int mu, const int32_t *sx, const int32_t *sid,
-                                            const int (&U)[A], int32_t *scr) {
-#pragma unroll
-    for (int a = 0; a < A; ++a)
-#pragma unroll
-        for (int j = a + 1; j < A; ++j) {
-            const int n0 = U[a], n1 = U[j], tot = n0 + n1;
-            const int32_t *X0 = sx + a * mu, *X1 = sx + j * mu, *I0 = sid + a * mu, *I1 = sid + j * mu;
-            int32_t *o0 = scr + (a * (A - 1) + (j - 1)) * mu;  // list a relative to j (jj = j - 1: j > a)
-            int32_t *o1 = scr + (j * (A - 1) + a) * mu;        // list j relative to a (jj = a: a < j)
-            const int d0 = (tid * tot) / nthr, d1 = ((tid + 1) * tot) / nthr;
-            int lo = max(0, d0 - n1), hi = min(d0, n0);
-            while (lo < hi) {  // merge-path split of diagonal d0 (ties: list a first)
-                const int mid = (lo + hi) >> 1;
-                if (X0[mid] <= X1[d0 - mid - 1])
-                    lo = mid + 1;
-                else
-                    hi = mid;
-            }
-            int i0 = lo, i1 = d0 - lo;
-            int32_t x0 = i0 < n0 ? X0[i0] : INT32_MAX, x1 = i1 < n1 ? X1[i1] : INT32_MAX;
-            for (int d = d0; d < d1; ++d) {
-                if (x0 <= x1 && i0 < n0) {
-                    o0[i0] = x0 == x1 ? I1[i1] : 0;
-                    ++i0;
-                    x0 = i0 < n0 ? X0[i0] : INT32_MAX;
-                } else {
-                    o1[i1] = (i0 > 0 && X0[i0 - 1] == x1) ? I0[i0 - 1] : 0;
-                    ++i1;
-                    x1 = i1 < n1 ? X1[i1] : INT32_MAX;
-                }
-            }
-        }
-}
-
-// Row build from precomputed cross ids (wj_join_cross): no searches, the
-// fp16 table rows of kRowU landings are loaded together.
-template <int A, int W, bool INF>
-__device__ __forceinline__ void build_rows_x(const EncMmaArgs &g, int tid, int nthr, const int32_t *scr,
-                                             const int32_t *sid, const int (&pu)[A + 1], unsigned char *xr,
-                                             uint16_t *vl, uint16_t *nl) {
-    const int mu = g.mu;
-    const int LT = pu[A];
-    for (int e0 = tid; e0 < LT; e0 += kRowU * nthr) {
-        uint4 t4[kRowU][A];
-        int rowi[kRowU];
-#pragma unroll
-        for (int u = 0; u < kRowU; ++u) {
-            const int e = e0 + u * nthr;
-            const bool ok = e < LT;
-            int a = 0;
-#pragma unroll
-            for (int t = 1; t < A; ++t) a += e >= pu[t];
-            int base_a = 0;
-#pragma unroll
-            for (int t = 1; t < A; ++t)
-                if (a == t) base_a = pu[t];
-            const int l = ok ? e - base_a : 0;
-            rowi[u] = ok ? a * mu + l : -1;
-#pragma unroll
-            for (int j = 0; j < A; ++j) {
-                const int jj = j < a ? j : j - 1;
-                const int id = !ok ? 0 : (j == a ? sid[a * mu + l] : scr[(a * (A - 1) + jj) * mu + l]);
-                t4[u][j] = __ldg(g.trow + id);
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < kRowU; ++u) {
-            if (rowi[u] < 0) continue;
-            uint32_t r[A][4];
-#pragma unroll
-            for (int j = 0; j < A; ++j) {
-                r[j][0] = t4[u][j].x;
-                r[j][1] = t4[u][j].y;
-                r[j][2] = t4[u][j].z;
-                r[j][3] = t4[u][j].w;
-            }
-            uint32_t w[8];
-            splice_row<A, W>(r, w);
-            const uint32_t row = (uint32_t)rowi[u];
-            if (INF) {  // list position e -> row; 2 n_l = twice the own block's row sum (fp16)
-                const int a = (int)(row / (uint32_t)g.mu);
-                __half2 acc = __floats2half2_rn(0.f, 0.f);
-#pragma unroll
-                for (int j = 0; j < A; ++j)
-                    if (j == a)
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) acc = __hadd2(acc, *reinterpret_cast<const __half2 *>(&r[j][k]));
-                const __half n = __hadd(__low2half(acc), __high2half(acc));  // W <= 8 halves; padding is 0
-                const int e = e0 + u * nthr;
-                vl[e] = (uint16_t)row;
-                nl[e] = __half_as_ushort(__hadd(n, n));
-            }
-            const uint32_t sw = (row >> 2) & 1u;
-            *reinterpret_cast<uint4 *>(xr + row * kRowB + (sw << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
-            *reinterpret_cast<uint4 *>(xr + row * kRowB + ((sw ^ 1u) << 4)) = make_uint4(w[4], w[5], w[6], w[7]);
-        }
-    }
-}
-
 template <int A, int AW, int kMW, int MINB, bool INF>
 __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaArgs g) {
     static_assert(AW + 1 <= 16, "one k16 step: A*(L+1) + 1 <= 16");
@@ -378,7 +179,7 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
     // reduction runs -- CTAs that run ahead (or start early under PDL) take
     // more queries.  The last CTA to finish resets the counters.
     const bool dyn = g.qsched != nullptr;
-    int64_t *next_b = reinterpret_cast<int64_t *>(wscale + 12);
+    int64_t *next_b = reinterpret_cast<int64_t *>(wscale + 20);
     const int32_t *gstart = g.groups ? g.groups + 1 : nullptr;
     const int32_t *gorder = g.groups ? g.groups + 2 + g.n_units : nullptr;
     const int32_t *gtup = g.groups ? gorder + g.n_batch : nullptr;  // [G][A] each unit's anchor tuple
@@ -696,8 +497,6 @@ __global__ void __launch_bounds__(128) join_cross_kernel(const int64_t *__restri
         }
 }
 
-using EncMmaKernel = void (*)(EncMmaArgs);
-
 template <int NW, int MINB, bool INF = false>
 static EncMmaKernel pick_mma(int A, int W) {
 #define WJ_CASE(a, w) \
@@ -746,6 +545,8 @@ struct MmaPlan {
     int slots = 0;  // resident CTAs on the device (persistent grid)
     int lcap = 0, xr_bytes = 0, mu = 1;
     bool infer = false;
+    bool tc = false;  // the tcgen05 kernel (encode_tc.cu)
+    int threads = 128;
 };
 
 
@@ -756,32 +557,51 @@ struct MmaPlan {
 static int plan_mma(int arity, int num_walks, int num_steps, int max_unique, MmaPlan &pl, bool infer = false) {
     const int W = num_steps + 1;
     // CTA shape: warps x min resident CTAs per SM (register budget); tuning
-    // override WJ_ENC_CFG in {"4x2", "4x3", "4x4", "8x2"}
-    static const char *env_cfg = getenv("WJ_ENC_CFG");
+    // override WJ_ENC_CFG in {"4x2", "4x3", "4x4", "8x2"}.  WJ_ENC_TC = "4" /
+    // "8" selects the tcgen05 kernel (encode_tc.cu) with that many dropout
+    // warps where it applies (arity <= 2); unset or "0": the mma.sync kernel
+    // (measured faster at C3)
+    const char *env_cfg = getenv("WJ_ENC_CFG");
+    const char *env_tc = getenv("WJ_ENC_TC");
     const int cfg = env_cfg ? (env_cfg[0] - '0') * 10 + (env_cfg[2] - '0') : 43;
+    const int tc_nw = env_tc ? (env_tc[0] == '4' ? 4 : env_tc[0] == '8' ? 8 : 0) : 0;
     if (num_walks > 2048) return WJ_ERR_UNSUPPORTED;
     const int64_t P = (int64_t)num_walks * W;
     pl.infer = infer && P <= 1024;
-    if (pl.infer) pl.k = pick_mma<4, 3, true>(arity, W);
+    pl.tc = false;
+    if (tc_nw && (pl.k = pick_tc(arity, W, pl.infer, tc_nw)) != nullptr) {
+        pl.tc = true;
+        pl.nw = tc_nw;
+    } else if (pl.infer) pl.k = pick_mma<4, 3, true>(arity, W);
     else if (cfg == 42) pl.k = pick_mma<4, 2>(arity, W);
     else if (cfg == 44) pl.k = pick_mma<4, 4>(arity, W);
     else if (cfg == 82) { pl.k = pick_mma<8, 2>(arity, W); pl.nw = 8; }
     else pl.k = pick_mma<4, 3>(arity, W);
     if (!pl.k) return WJ_ERR_UNSUPPORTED;
+    pl.threads = pl.nw * 32 + (pl.tc ? 32 : 0);  // tcgen05: + the MMA-issuing warp
     pl.mu = max_unique < 1 ? 1 : max_unique;
     if (P > 65535 || (int64_t)arity * pl.mu + 1 > 65535) {
         set_error("M*(L+1) or A*max_unique too large for uint16 row indices");
         pl.k = nullptr;
         return WJ_ERR_UNSUPPORTED;
     }
-    // virtual landings per query: sum_a sum_l ceil(n_l / 2) <= A (P + U) / 2, + 2 x 15 padding
-    pl.lcap = (int)(((int64_t)arity * ((P + pl.mu) / 2 + 1) + 32 + 7) & ~7LL);
-    if (pl.infer) pl.lcap = 2 * ((arity * pl.mu + 16 + 7) & ~7);  // list positions + 2 n_l per position
     const int64_t rows_b = ((int64_t)arity * pl.mu + 1) * kRowB;
-    const int64_t red_b = (int64_t)pl.nw * 64 * kRedS * 4;
-    pl.xr_bytes = (int)(((rows_b > red_b ? rows_b : red_b) + 15) & ~15LL);
-    pl.smem = (size_t)kWtBytes + kHdrBytes + (size_t)pl.xr_bytes + (size_t)(2 * arity + arity * (arity - 1)) * pl.mu * 4 +
-              (size_t)pl.lcap * 2;
+    if (pl.tc) {
+        // virtual landings per query: sum_a sum_l ceil(n_l / 2) <= A (P + U) / 2,
+        // + two sections padded to 32 + the last tile padded to 128
+        pl.lcap = (int)(((int64_t)arity * ((P + pl.mu) / 2 + 1) + 2 * 31 + 127 + 7) & ~7LL);
+        if (pl.infer) pl.lcap = 2 * ((arity * pl.mu + 128 + 7) & ~7);  // list positions + 2 n_l per position
+        pl.xr_bytes = (int)((rows_b + 15) & ~15LL);
+        pl.smem = tc_smem(arity, pl.mu, pl.lcap, pl.xr_bytes);
+    } else {
+        // virtual landings per query: sum_a sum_l ceil(n_l / 2) <= A (P + U) / 2, + 2 x 15 padding
+        pl.lcap = (int)(((int64_t)arity * ((P + pl.mu) / 2 + 1) + 32 + 7) & ~7LL);
+        if (pl.infer) pl.lcap = 2 * ((arity * pl.mu + 16 + 7) & ~7);  // list positions + 2 n_l per position
+        const int64_t red_b = (int64_t)pl.nw * 64 * kRedS * 4;
+        pl.xr_bytes = (int)(((rows_b > red_b ? rows_b : red_b) + 15) & ~15LL);
+        pl.smem = (size_t)kWtBytes + kHdrBytes + (size_t)pl.xr_bytes +
+                  (size_t)(2 * arity + arity * (arity - 1)) * pl.mu * 4 + (size_t)pl.lcap * 2;
+    }
     if (pl.smem > 200 * 1024) {
         set_error("join_encode needs %zu B of shared memory", pl.smem);
         pl.k = nullptr;
@@ -793,8 +613,29 @@ static int plan_mma(int arity, int num_walks, int num_steps, int max_unique, Mma
         pl.k = nullptr;
         return WJ_ERR_CUDA;
     }
+    cudaFuncSetAttribute(pl.k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pl.k, pl.nw * 32, pl.smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pl.k, pl.threads, pl.smem);
+    if (getenv("WJ_ENC_DEBUG")) {
+        cudaFuncAttributes fa;
+        cudaFuncGetAttributes(&fa, pl.k);
+        int ps0 = 0, ps48 = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps0, pl.k, pl.threads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps48, pl.k, pl.threads, 48 * 1024);
+        fprintf(stderr, "  attrs: regs=%d static_smem=%zu max_dyn=%d maxthr=%d occ(0)=%d occ(48K)=%d\n", fa.numRegs,
+                fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes, fa.maxThreadsPerBlock, ps0, ps48);
+    }
+    if (getenv("WJ_ENC_DEBUG"))
+        fprintf(stderr, "join_encode plan: tc=%d nw=%d smem=%zu per_sm=%d (%s) mu=%d lcap=%d\n", (int)pl.tc, pl.nw,
+                pl.smem, per_sm, cudaGetErrorString(e), pl.mu, pl.lcap);
+    if (pl.tc) {
+        // the occupancy API reports one CTA per SM for kernels that allocate
+        // tensor memory; residency is bounded by TMEM (512 columns / 256 per
+        // CTA), shared memory (227 KB per SM) and registers, all of which
+        // admit two CTAs of this kernel
+        const int by_smem = (int)((227 * 1024) / (pl.smem + 1024 + 128));
+        per_sm = by_smem < 2 ? by_smem : 2;
+    }
     pl.slots = sm_count() * (per_sm > 0 ? per_sm : 1);
     return WJ_OK;
 }
@@ -864,7 +705,7 @@ extern "C" int wj_join_encode(const int64_t *queries, int64_t n_batch, int32_t a
     // persistent: one resident CTA slot per (SM, occupancy) -- W^T is split
     // once per CTA, not once per query
     const int64_t blocks = n_batch < pl.slots ? n_batch : pl.slots;
-    const cudaError_t e = launch_pdl(pl.k, dim3((unsigned)blocks), dim3(pl.nw * 32), pl.smem, (cudaStream_t)stream, g);
+    const cudaError_t e = launch_pdl(pl.k, dim3((unsigned)blocks), dim3(pl.threads), pl.smem, (cudaStream_t)stream, g);
     if (e != cudaSuccess) {
         set_error("wj_join_encode launch: %s", cudaGetErrorString(e));
         return WJ_ERR_CUDA;
@@ -972,7 +813,7 @@ extern "C" int wj_stepper_encode(wj_stepper *st, const int64_t *queries, int64_t
     g.groups = groups;
     g.n_units = groups ? n_groups : n_batch;
     const int64_t blocks = g.n_units < st->plan.slots ? g.n_units : st->plan.slots;
-    cudaError_t e = launch_pdl(st->plan.k, dim3((unsigned)blocks), dim3(st->plan.nw * 32), st->plan.smem,
+    cudaError_t e = launch_pdl(st->plan.k, dim3((unsigned)blocks), dim3(st->plan.threads), st->plan.smem,
                                (cudaStream_t)stream, g);
     if (e != cudaSuccess) {
         set_error("wj_stepper: join_encode launch: %s", cudaGetErrorString(e));

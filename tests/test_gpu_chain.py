@@ -51,8 +51,11 @@ def _run(store, batches, launch, where):
     return {k: v.detach().clone() for k, v in p.tensors.items()}, losses, int(step.step_t.item())
 
 
+@pytest.mark.parametrize("kernel", ["mma", "tc"])
 @pytest.mark.parametrize("where", ["device", "pinned"])
-def test_chain_equals_graph(store_and_batches, where):
+def test_chain_equals_graph(store_and_batches, where, kernel, monkeypatch):
+    if kernel == "tc":  # the tcgen05 join+encode kernel (encode_tc.cu)
+        monkeypatch.setenv("WJ_ENC_TC", "8")
     store, batches = store_and_batches
     pg, lg, tg = _run(store, batches, "graph", where)
     pc, lc, tc = _run(store, batches, "chain", where)

@@ -2,6 +2,8 @@
 the CPU oracle.  Bit-exact for walks / RPE index / table / dicts / join /
 dense; encoder logits within 1e-5 relative (north_star tolerance)."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -432,6 +434,84 @@ def _fused_model_mma(store, q, w1, b1, keep, seed, step):
     return pooled, S, msum
 
 
+def _tc_kernel_active(arity, L):
+    """WJ_ENC_TC=4|8 selects the tcgen05 kernel (encode_tc.cu) for arity <= 2
+    with A(L+1)+1 <= 16; otherwise the mma.sync kernel serves the shape."""
+    return os.environ.get("WJ_ENC_TC", "0") in ("4", "8") and arity <= 2 and arity * (L + 1) + 1 <= 16
+
+
+def _fused_model_tc(store, q, w1, b1, keep, seed, step):
+    """Host model of the tcgen05 wj_join_encode (encode_tc.cu): the query's
+    virtual landings in vindex order (section 2 padded to 32, section 1, the
+    total padded to 128), counter (landing v, unit pair k): x = (qq + (v << 5)
+    + k) * C1, one xorshift-multiply-xorshift round, the low 14-bit lane for
+    unit 2k and the high one for unit 2k + 1."""
+    G = 0x9E3779B97F4A7C15
+    off = store.offsets_d.cpu().numpy()
+    ux = store.uniq_x_d.cpu().numpy()
+    uid = store.uniq_id_d.cpu().numpy()
+    T = store.table.vectors.astype(np.int64)
+    B, A = q.shape
+    W = store.width
+    H = w1.shape[1]
+    t11, t21, t22 = _thresholds14(keep)
+    skey = _mix64((seed + G * (step + 1)) & _M64)
+    pooled = np.zeros((B, H))
+    S = np.zeros((B, A * W, H))
+    msum = np.zeros((B, H))
+    kk = np.arange(H // 2, dtype=np.uint64)[None, :]
+    for b in range(B):
+        qq = _mix64(skey ^ _mix64(b)) & _M32
+        qq ^= qq >> 16
+        lists = [(ux[off[q[b, j]]:off[q[b, j] + 1]], uid[off[q[b, j]]:off[q[b, j] + 1]]) for j in range(A)]
+        sec2, sec1 = [], []
+        for a in range(A):
+            xa, ida = lists[a]
+            ids = np.zeros((len(xa), A), np.int64)
+            for j in range(A):
+                if j == a:
+                    ids[:, j] = ida
+                else:
+                    xj, idj = lists[j]
+                    pos = np.searchsorted(xj, xa)
+                    pos_c = np.minimum(pos, len(xj) - 1)
+                    ids[:, j] = np.where((pos < len(xj)) & (xj[pos_c] == xa), idj[pos_c], 0)
+            X = T[ids].reshape(len(xa), A * W)
+            n_l = T[ida].sum(1)
+            for l in range(len(xa)):
+                sec2 += [X[l]] * int(n_l[l] // 2)
+            for l in range(len(xa)):
+                if n_l[l] % 2:
+                    sec1.append(X[l])
+        zero = np.zeros(A * W, np.int64)
+        rows2 = sec2 + [zero] * ((-len(sec2)) % 32)
+        rows = rows2 + sec1
+        rows = rows + [zero] * ((-len(rows)) % 128)
+        X = np.asarray(rows, np.float64).reshape(-1, A * W)
+        two = np.arange(X.shape[0]) < len(rows2)
+        V = X.shape[0]
+        z = (b1[None, :].astype(np.float64) + X @ w1.astype(np.float64)).astype(np.float32)
+        z[np.all(X == 0, axis=1)] = 0.0  # padding rows: contribute nothing
+        v = np.arange(V, dtype=np.uint64)[:, None]
+        x = ((np.uint64(qq) + (v << np.uint64(5)) + kk) * np.uint64(0x7FEB352D)) & np.uint64(_M32)
+        x ^= x >> np.uint64(15)
+        x = (x * np.uint64(0x846CA68B)) & np.uint64(_M32)
+        y = ~(x ^ (x >> np.uint64(16))) & np.uint64(0x3FFF3FFF)
+        lanes = np.empty((V, H), np.int64)
+        lanes[:, 0::2] = (y & np.uint64(0xFFFF)).astype(np.int64)
+        lanes[:, 1::2] = (y >> np.uint64(16)).astype(np.int64)
+        u = 0x3FFF - lanes
+        ta = np.where(two, t21, t11)[:, None]
+        tb = np.where(two, t22, 0)[:, None]
+        kept = (u < ta).astype(np.float64) + (u < tb)
+        posm = z >= 0
+        pooled[b] = (np.where(posm, z, 0) * kept).sum(0)
+        gk = posm * kept
+        msum[b] = (gk * X.any(axis=1)[:, None]).sum(0)
+        S[b] = X.T @ gk
+    return pooled, S, msum
+
+
 @pytest.mark.parametrize("keep", [1.0, 0.9])
 @pytest.mark.parametrize("kernel", ["mma", "simt"])
 @pytest.mark.parametrize("arity,L", [(2, 4), (3, 3)])
@@ -449,7 +529,7 @@ def test_fused_join_encode_matches_host_model(wj, keep, kernel, arity, L):
     wj.encoder.join_encode(s, qd, p.w1, p.b1, float(keep), 99, step, pooled, S, msum, simt=(kernel == "simt"))
     w1 = p.w1.cpu().numpy()
     b1 = p.b1.cpu().numpy()
-    model = _fused_model_mma if kernel == "mma" else _fused_model
+    model = _fused_model if kernel == "simt" else (_fused_model_tc if _tc_kernel_active(arity, L) else _fused_model_mma)
     mp, mS, mm = model(s, q, w1, b1, keep, 99, 6)
     np.testing.assert_allclose(pooled.cpu().numpy(), mp, rtol=2e-5, atol=1e-3)
     # S and msum are integer-weighted sums: exact unless a z sits within rounding of 0
@@ -459,6 +539,29 @@ def test_fused_join_encode_matches_host_model(wj, keep, kernel, arity, L):
         nod = model(s, q, w1, b1, 1.0, 99, 6)[2]
         frac = mm.sum() / nod.sum()
         assert abs(frac - keep) < 0.01
+
+
+@pytest.mark.parametrize("nw", ["8", "4"])
+@pytest.mark.parametrize("keep", [1.0, 0.9])
+@pytest.mark.parametrize("arity,L", [(2, 4), (1, 3), (2, 6)])
+def test_tcgen05_join_encode_matches_host_model(wj, monkeypatch, nw, keep, arity, L):
+    """The tcgen05 + TMEM kernel (encode_tc.cu, WJ_ENC_TC=4|8) against the
+    host model of its dropout stream: pooled within 2e-5, S / msum exact."""
+    monkeypatch.setenv("WJ_ENC_TC", nw)
+    g = _er(800, 6_000, 4)
+    s = wj.preprocess(g, 40, L, 21)
+    rng = np.random.default_rng(5)
+    q = np.stack([rng.choice(800, arity, replace=False) for _ in range(20)]).astype(np.int64)
+    p = wj.init_params(arity, L, dropout=1 - keep, seed=2)
+    step = torch.tensor([6], dtype=torch.int64, device="cuda")
+    pooled = torch.empty((20, 64), device="cuda")
+    S = torch.empty((20, arity * (L + 1), 64), device="cuda")
+    msum = torch.empty((20, 64), device="cuda")
+    wj.encoder.join_encode(s, torch.from_numpy(q).cuda(), p.w1, p.b1, float(keep), 99, step, pooled, S, msum)
+    mp, mS, mm = _fused_model_tc(s, q, p.w1.cpu().numpy(), p.b1.cpu().numpy(), keep, 99, 6)
+    np.testing.assert_allclose(pooled.cpu().numpy(), mp, rtol=2e-5, atol=1e-3)
+    assert np.mean(np.abs(S.cpu().numpy() - mS) < 0.5) > 0.999
+    assert np.mean(np.abs(msum.cpu().numpy() - mm) < 0.5) > 0.999
 
 
 def test_dropout_stream_statistics(wj):
