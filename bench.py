@@ -1,28 +1,46 @@
 #!/usr/bin/env python
 """Benchmark of the walk -> RPE -> join -> encode hot path (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3|c2|c1]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3|c2|c1|c5a|c5b|c4] [--what train|infer]
     python bench.py --impl reference ...      # CPU reference arm (oracle port)
 
-Workload (default c3 = BASELINE.json configs[2], the metric's citation2 shape):
-Erdos-Renyi graph with 2,927,963 nodes / 30,561,187 edges, 5% of the edges
-held out as training positives and removed from the walk graph, M=200 walks
-of L=4 steps, link queries (A=2), reference batches of 32 positives + 50
-in-seed negatives each (1,632 queries).  Synthetic data, random-init encoder.
+Workloads (synthetic data of the named shapes, random-init
+encoder):
+* c3 (default) = BASELINE.json configs[2], the metric's citation2 shape:
+  Erdos-Renyi graph 2,927,963 nodes / 30,561,187 edges, 5% of the edges held
+  out as training positives and removed from the walk graph, M=200 walks of
+  L=4 steps, link queries (A=2), reference batches of 32 positives + 50
+  in-seed negatives each (1,632 queries).
+* c1 = configs[0] (10K / 100K, M=50, L=3), c2 = configs[1] (collab shape,
+  235,868 / 1,285,465, M=200, L=4), c5b = configs[4] vessel shape (3,538,495 /
+  5,345,897, degree ~3, ~5% isolated anchors, M=200, L=4), c5a = configs[4]
+  tags-math shape (1,629 nodes / 91,685 projected edges, 74,955 triplet
+  hyperedges as A=3 training positives, k_neg=10, M=100, L=3), c4 =
+  configs[3] ogb-mag P-A shape (736,389 papers + 1,134,649 authors, 7,145,660
+  P-A + 5,416,271 P-P typed edges, metapath P->A, A->P, P->A walks, M=200,
+  L=3, (paper, author) relation queries, k_neg=10).
 
-A "step" is one training batch: join+densify kernel -> encoder forward ->
-BCE -> backward -> Adam (one captured CUDA graph).  The metric is the
-reference's train q/s: Q_epoch / (t_pre + batches_per_epoch * t_step), with
-t_pre the device time of the full preprocess (sample + RPE + intern, run in
-this process) and t_step the mean device time of K timed steps.
-``value`` takes queries resident in HBM; ``e2e`` feeds every step from
-pinned host memory (H2D of the batch, D2H of the loss inside the timed
-region) and preprocesses from the host CSR.
+--what train (default): a "step" is one training batch through the step
+executor (join+encode -> tail -> Adam, one PDL chain across steps).  The
+metric is the reference's train q/s: Q_epoch / (t_pre + batches_per_epoch *
+t_step), t_pre the device time of the full preprocess in this process and
+t_step the mean device time of K timed steps (inputs resident in HBM).
+``e2e`` runs one FULL epoch from host data: host CSR -> preprocess, the
+native batch planner on its producer thread -> pinned batches -> H2D -> step
+-> loss to pinned host memory, every batch of the epoch timed.
+
+--what infer: a "step" scores one chunk of 16 test positives, each with 1,000
+negatives sharing its first node (100 at c5a), i.e. 16,016
+queries, through the fused scorer (join+encode at keep = 1, logits tail).
+``e2e`` goes through ``score_array`` from pinned host queries and reads the
+scores back every step.
 """
 
 from __future__ import annotations
 
 import argparse
+import glob
+import hashlib
 import json
 import math
 import os
@@ -38,14 +56,23 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIGS = {
-    "c3": dict(workload="ogbl-citation2-shape", n=2_927_963, m=30_561_187, M=200, L=4, A=2,
-               ubar=528.5),
-    "c2": dict(workload="ogbl-collab-shape", n=235_868, m=1_285_465, M=200, L=4, A=2, ubar=393.1),
-    "c1": dict(workload="er-10k", n=10_000, m=100_000, M=50, L=3, A=2, ubar=106.8),
+    "c3": dict(kind="link", workload="ogbl-citation2-shape", n=2_927_963, m=30_561_187, M=200, L=4, A=2, k_neg=50,
+               baseline_cfg=2),
+    "c2": dict(kind="link", workload="ogbl-collab-shape", n=235_868, m=1_285_465, M=200, L=4, A=2, k_neg=50,
+               baseline_cfg=1),
+    "c1": dict(kind="link", workload="er-10k", n=10_000, m=100_000, M=50, L=3, A=2, k_neg=50, baseline_cfg=0),
+    "c5b": dict(kind="link", workload="ogbl-vessel-shape", n=3_538_495, m=5_345_897, M=200, L=4, A=2, k_neg=50,
+                baseline_cfg=4),
+    "c5a": dict(kind="hyper", workload="tags-math-shape", n=1_629, m=91_685, hyperedges=74_955, M=100, L=3, A=3,
+                k_neg=10, infer_neg=100, baseline_cfg=4),
+    "c4": dict(kind="typed", workload="ogb-mag-P-A-shape", papers=736_389, authors=1_134_649, pa=7_145_660,
+               pp=5_416_271, M=200, L=3, A=2, k_neg=10, metapath=[1, 2, 1], baseline_cfg=3),
 }
-TRAIN_FRAC, K_NEG, POS_PER_BATCH = 0.05, 50, 32
+TRAIN_FRAC, POS_PER_BATCH = 0.05, 32
 GRAPH_SEED, STORE_SEED, BATCH_SEED = 1, 3, 7
+INFER_POS_PER_STEP, INFER_NEG = 16, 1000
 METRIC = "train queries/sec (sample+RPE+join+encode) on citation2-shape; HBM GB/s"
+METRIC_INFER = "inference queries/sec (join+encode scoring, 1 positive : 1000 negatives)"
 
 
 def parse():
@@ -55,8 +82,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--what", default="train", choices=["train", "infer"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--no-epoch", action="store_true", help="e2e over K steps instead of one full epoch")
     ap.add_argument("--cpu-shard-nodes", type=int, default=0, help="0 = auto")
     ap.add_argument("--pre", default="sharded", choices=["sharded", "redundant"],
                     help="N>1 preprocess: node-range shards + NCCL all-gathers, or the full store on every rank "
@@ -75,6 +104,45 @@ def peaks():
         return float(p["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def kernel_source_hash() -> str:
+    """sha256 over the CUDA / C++ sources: ties an ncu capture to the build."""
+    h = hashlib.sha256()
+    for f in sorted(glob.glob(os.path.join(ROOT, "paper_2202_13538_b200", "csrc", "*"))):
+        with open(f, "rb") as fh:
+            h.update(os.path.basename(f).encode() + b"\0" + fh.read())
+    return h.hexdigest()[:16]
+
+
+def ncu_capture(config: str, kernel: str):
+    """The committed ncu summary of ``kernel`` at ``config`` (written by
+    profiles/ncu_summary.py from one ncu --set full capture) and whether it was
+    taken from these exact sources."""
+    path = os.path.join(ROOT, "profiles", f"{config}_{kernel}_ncu.json")
+    if not os.path.exists(path):
+        return None, False
+    try:
+        d = json.load(open(path))
+    except Exception:
+        return None, False
+    return d, d.get("src_sha") == kernel_source_hash()
+
+
+def b_q_baseline(cfg, ubar, n, q_epoch):
+    """BASELINE.md §2 algorithmic bytes per training query (s = 2 B)."""
+    M, L, A = cfg["M"], cfg["L"], cfg["A"]
+    c = 1 if M <= 255 else 2
+    b_pre = M * L * 64 + 2 * M * (L + 1) * 4 + ubar * (4 + c * (L + 1))
+    return (A * M * (L + 1) * 4 + A * ubar * (4 + c * (L + 1)) + 3 * A * A * M * (L + 1) ** 2 * 2
+            + b_pre * n / q_epoch)
+
+
+def join_bytes_q(cfg, ubar, s):
+    """SURVEY §8(d) join bytes per query (dense elements of s bytes)."""
+    M, L, A = cfg["M"], cfg["L"], cfg["A"]
+    c = 1 if M <= 255 else 2
+    return A * M * (L + 1) * 4 + A * ubar * (4 + c * (L + 1)) + A * A * M * (L + 1) ** 2 * s
 
 
 # ------------------------------------------------------------------ clocks --
@@ -138,29 +206,145 @@ def dist_env():
     return world, rank, local
 
 
-def build_inputs(cfg, device):
-    """Synthetic walk graph + training positives + batch plan (host)."""
-    from paper_2202_13538_b200.graph import synthetic_link_graph
-    from paper_2202_13538_b200.pipeline import PositiveFilter, QueryOverlapIndex
+class Workload:
+    """Walk graph (device), training positives and the positive filter (host),
+    and the preprocess of the config (homogeneous or metapath walks)."""
 
-    split = synthetic_link_graph(cfg["n"], cfg["m"], TRAIN_FRAC, seed=GRAPH_SEED, device=device)
-    index = QueryOverlapIndex(split.train_pos)
-    filt = PositiveFilter.__new__(PositiveFilter)
-    filt.n, filt.keys = cfg["n"], split.all_edges
-    return split, index, filt
+    def __init__(self, cfg, walk_graph, train_pos, filter_rows, edge_types=None, desc=""):
+        self.cfg = cfg
+        self.walk_graph = walk_graph
+        self.train_pos = np.ascontiguousarray(train_pos, dtype=np.int64)
+        self.filter_rows = np.ascontiguousarray(filter_rows, dtype=np.int64)
+        self.edge_types = edge_types  # device uint8 per CSR entry (c4) or None
+        self.n = int(walk_graph.num_nodes)
+        self.desc = desc
+
+    def prep(self, g, phases=None, sharded=False):
+        import paper_2202_13538_b200 as wj
+
+        cfg = self.cfg
+        if self.edge_types is not None:
+            return wj.preprocess_typed(g, self.edge_types, cfg["metapath"], cfg["M"], cfg["L"], STORE_SEED,
+                                       num_types=4)
+        if sharded:
+            from paper_2202_13538_b200.distributed import preprocess_sharded
+
+            return preprocess_sharded(g, cfg["M"], cfg["L"], STORE_SEED, phases=phases)
+        return wj.preprocess(g, cfg["M"], cfg["L"], STORE_SEED, phases=phases)
 
 
-def make_plan(split, index, filt, count, seed):
-    from paper_2202_13538_b200.pipeline import TrainConfig, make_batch
+def _unique_pairs(lo_n, hi_n, count, gen, dev, canon=True, lo_off=0, hi_off=0):
+    """``count`` distinct (a, b) pairs, a uniform in [lo_off, lo_off + lo_n),
+    b in [hi_off, hi_off + hi_n), a != b; canonical lo < hi keys if canon."""
+    import torch
 
-    tc = TrainConfig(batch_size=POS_PER_BATCH, k_neg=K_NEG)
+    n_all = lo_off + lo_n + hi_off + hi_n
+    keys = torch.empty(0, dtype=torch.int64, device=dev)
+    while keys.numel() < count:
+        k = int(count * 1.05) + 1024
+        a = torch.randint(0, lo_n, (k,), device=dev, generator=gen) + lo_off
+        b = torch.randint(0, hi_n, (k,), device=dev, generator=gen) + hi_off
+        ok = a != b
+        a, b = a[ok], b[ok]
+        if canon:
+            a, b = torch.minimum(a, b), torch.maximum(a, b)
+        keys = torch.unique(torch.cat([keys, a * n_all + b]))
+    keys = keys[torch.randperm(keys.numel(), device=dev, generator=gen)[:count]]
+    return torch.div(keys, n_all, rounding_mode="floor"), keys % n_all
+
+
+def build_workload(cfg, dev) -> Workload:
+    import torch
+
+    from paper_2202_13538_b200.graph import DeviceGraph, _csr_from_canonical, synthetic_link_graph
+
+    if cfg["kind"] == "link":
+        split = synthetic_link_graph(cfg["n"], cfg["m"], TRAIN_FRAC, seed=GRAPH_SEED, device=dev)
+        n = cfg["n"]
+        filt = np.stack([split.all_edges // n, split.all_edges % n], 1)
+        return Workload(cfg, split.walk_graph, split.train_pos, filt,
+                        desc=f"ER n={n} m={cfg['m']}, 5% link split")
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(GRAPH_SEED)
+    if cfg["kind"] == "hyper":
+        n = cfg["n"]
+        # the projected graph (all edges walkable) + uniform distinct triplets as hyperedges
+        split = synthetic_link_graph(n, cfg["m"], 1.0 / cfg["m"], seed=GRAPH_SEED, device=dev)
+        rows = torch.randint(0, n, (int(cfg["hyperedges"] * 1.3), 3), device=dev, generator=gen)
+        ok = (rows[:, 0] != rows[:, 1]) & (rows[:, 0] != rows[:, 2]) & (rows[:, 1] != rows[:, 2])
+        rows = torch.sort(rows[ok], dim=1).values
+        keys = torch.unique((rows[:, 0] * n + rows[:, 1]) * n + rows[:, 2])
+        keys = keys[torch.randperm(keys.numel(), device=dev, generator=gen)[:cfg["hyperedges"]]]
+        tri = torch.stack([keys // (n * n), (keys // n) % n, keys % n], 1).cpu().numpy()
+        return Workload(cfg, split.walk_graph, tri, tri,
+                        desc=f"ER projected graph n={n} m={cfg['m']}, {cfg['hyperedges']} triplet hyperedges")
+    # typed (c4): papers [0, P), authors [P, P + A); P-A and P-P edges; 5% of
+    # P-A held out as (paper, author) relation positives
+    P, Au = cfg["papers"], cfg["authors"]
+    n = P + Au
+    pa_a, pa_b = _unique_pairs(P, Au, cfg["pa"], gen, dev, canon=False, hi_off=P)
+    pp_a, pp_b = _unique_pairs(P, P, cfg["pp"], gen, dev)
+    perm = torch.randperm(cfg["pa"], device=dev, generator=gen)
+    n_train = int(round(TRAIN_FRAC * cfg["pa"]))
+    tr, rest = perm[:n_train], perm[n_train:]
+    lo = torch.cat([pa_a[rest], pp_a])
+    hi = torch.cat([pa_b[rest], pp_b])
+    idxptr, indices = _csr_from_canonical(lo, hi, n)
+    g = DeviceGraph(n, idxptr, indices)
+    deg = idxptr[1:] - idxptr[:-1]
+    rows = torch.repeat_interleave(torch.arange(n, device=dev), deg)
+    nt = lambda x: (x >= P).to(torch.uint8)  # noqa: E731  node type: 0 paper, 1 author
+    et = nt(rows) * 2 + nt(indices.long())     # relation type a*2 + b: P->P 0, P->A 1, A->P 2
+    train_pos = torch.stack([pa_a[tr], pa_b[tr]], 1).cpu().numpy()
+    filt = torch.cat([torch.stack([pa_a, pa_b], 1), torch.stack([pp_a, pp_b], 1)]).cpu().numpy()
+    return Workload(cfg, g, train_pos, filt, edge_types=et,
+                    desc=f"typed: {P} papers + {Au} authors, {cfg['pa']} P-A + {cfg['pp']} P-P edges, "
+                         f"5% of P-A held out, metapath {cfg['metapath']} (P->A, A->P, P->A)")
+
+
+def build_inputs(cfg, dev):
+    """Profiling scripts' entry (profiles/*.py): (workload, None, None)."""
+    return build_workload(cfg, dev), None, None
+
+
+def make_plan(wl, *rest):
+    """``count`` reference training batches: make_plan(wl, count, seed) (the
+    profiling scripts' make_plan(wl, index, filt, count, seed) also works)."""
+    from paper_2202_13538_b200.pipeline import PositiveFilter, QueryOverlapIndex, TrainConfig, make_batch
+
+    count, seed = rest[-2], rest[-1]
+
+    tc = TrainConfig(batch_size=POS_PER_BATCH, k_neg=wl.cfg["k_neg"])
+    index = QueryOverlapIndex(wl.train_pos)
+    filt = PositiveFilter(wl.filter_rows, wl.n)
     rng = np.random.default_rng(seed)
-    return [make_batch(index, split.train_pos, filt, tc, rng) for _ in range(count)]
+    return [make_batch(index, wl.train_pos, filt, tc, rng) for _ in range(count)]
 
 
-def epoch_shape(split):
-    n_pos = int(split.train_pos.shape[0])
-    return n_pos * (1 + K_NEG), math.ceil(n_pos / POS_PER_BATCH)
+def epoch_shape(wl):
+    n_pos = int(wl.train_pos.shape[0])
+    return n_pos * (1 + wl.cfg["k_neg"]), math.ceil(n_pos / POS_PER_BATCH)
+
+
+def infer_queries(wl, steps, seed):
+    """Scoring chunks: 16 positives per step, each followed by its negatives
+    (the positive's first A-1 nodes + a uniform random last node)."""
+    rng = np.random.default_rng(seed)
+    k = wl.cfg.get("infer_neg", INFER_NEG)
+    out = []
+    for s in range(steps):
+        pos = wl.train_pos[rng.integers(0, wl.train_pos.shape[0], INFER_POS_PER_STEP)]
+        rows = []
+        for p in pos:
+            neg = np.repeat(p[None, :], k, 0)
+            last = rng.integers(0, wl.n, k)
+            clash = np.any(neg[:, :-1] == last[:, None], axis=1)
+            last[clash] = (last[clash] + 1) % wl.n
+            neg[:, -1] = last
+            rows.append(p[None, :])
+            rows.append(neg)
+        out.append(np.ascontiguousarray(np.concatenate(rows), dtype=np.int64))
+    return out
 
 
 # --------------------------------------------------------------- our arm --
@@ -171,7 +355,6 @@ def run_ours(args, cfg):
 
     import paper_2202_13538_b200 as wj
     from paper_2202_13538_b200 import _lib
-    from paper_2202_13538_b200.joiner import dense_batch
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -180,7 +363,6 @@ def run_ours(args, cfg):
         dist.init_process_group("nccl", device_id=dev)
     _lib.load()
     torch.manual_seed(1234 + rank)
-    M, L, A = cfg["M"], cfg["L"], cfg["A"]
 
     def barrier_sync():
         if world > 1:
@@ -194,49 +376,78 @@ def run_ours(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    split, index, filt = build_inputs(cfg, dev)
-    q_epoch, nb_epoch = epoch_shape(split)
-    g = split.walk_graph
+    wl = build_workload(cfg, dev)
+    g = wl.walk_graph
+    sharded = world > 1 and args.pre == "sharded" and wl.edge_types is None
 
     # ---- preprocess: warm once, then time the full Alg. 1 on device
-    if world > 1 and args.pre == "sharded":
-        from paper_2202_13538_b200.distributed import preprocess_sharded as prep
-    else:
-        prep = wj.preprocess
-    store = prep(g, M, L, STORE_SEED)
+    store = wl.prep(g, sharded=sharded)
     del store  # its blocks stay in the caching allocator: the timed run measures device work
     phases = []
     barrier_sync()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    store = prep(g, M, L, STORE_SEED, phases=phases)
+    store = wl.prep(g, phases=phases, sharded=sharded)
     e1.record()
     barrier_sync()
     t_pre = max_over_ranks(e0.elapsed_time(e1) / 1e3)
     phase_ms = {name: a.elapsed_time(b) for name, a, b in phases}
     ubar = store.num_entries / store.num_nodes
+    ctx = dict(world=world, rank=rank, local=local, dev=dev, barrier_sync=barrier_sync,
+               max_over_ranks=max_over_ranks, t_pre=t_pre, phase_ms=phase_ms, ubar=ubar, wl=wl)
+    if args.what == "infer":
+        return run_ours_infer(args, cfg, store, ctx)
+    return run_ours_train(args, cfg, store, ctx)
+
+
+def _common_config(cfg, wl, store, ctx, extra):
+    out = {"workload": f"{cfg['workload']} ({wl.desc}), M={cfg['M']}, L={cfg['L']}, A={cfg['A']}",
+           "config": [k for k, v in CONFIGS.items() if v is cfg][0],
+           "baseline_json_config": cfg["baseline_cfg"], "n_nodes": wl.n,
+           "walk_graph_edges": int(wl.walk_graph.indices.numel() // 2), "M": cfg["M"], "L": cfg["L"],
+           "arity": cfg["A"], "t_pre_ms": round(ctx["t_pre"] * 1e3, 3),
+           "t_pre_phase_ms": {k: round(v, 3) for k, v in ctx["phase_ms"].items()},
+           "store_entries": int(store.num_entries), "ubar_measured": round(ctx["ubar"], 2),
+           "table_size": int(store.table_keys_d.numel()),
+           "l2": "inputs larger than L2 for c3/c5b/c4 (store > 10 GB, a different random batch every step); "
+                 "c1/c2/c5a stores partly L2-resident"}
+    out.update(extra)
+    return out
+
+
+def run_ours_train(args, cfg, store, ctx):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2202_13538_b200 as wj
+    from paper_2202_13538_b200 import _lib
+    from paper_2202_13538_b200.joiner import dense_batch
+    from paper_2202_13538_b200.pipeline import GROUP_MAX
+
+    world, rank, local, dev = ctx["world"], ctx["rank"], ctx["local"], ctx["dev"]
+    barrier_sync, max_over_ranks = ctx["barrier_sync"], ctx["max_over_ranks"]
+    wl, t_pre, ubar = ctx["wl"], ctx["t_pre"], ctx["ubar"]
+    M, L, A = cfg["M"], cfg["L"], cfg["A"]
+    q_epoch, nb_epoch = epoch_shape(wl)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
     # ---- batch plan (host), uploaded before the timed region
     W, K = args.warmup, args.steps
-    plan = make_plan(split, index, filt, W + K, BATCH_SEED + rank)
+    plan = make_plan(wl, W + K, BATCH_SEED + rank)
     qd = [torch.from_numpy(q).to(dev) for q, _ in plan]
     yd = [torch.from_numpy(y).to(dev) for _, y in plan]
-    # the planner's per-batch groups of identical queries (wj_group_queries),
-    # resident with their batch
-    from paper_2202_13538_b200.pipeline import GROUP_MAX
-
-    gd = []
+    gd = []  # the planner's per-batch groups of identical queries (wj_group_queries)
     for q, _ in plan:
         gb = np.empty((2 + q.shape[1]) * q.shape[0] + 2, dtype=np.int32)
         _lib.call("wj_group_queries", q.ctypes.data, q.shape[0], q.shape[1], GROUP_MAX, gb.ctypes.data, None)
         gd.append((torch.from_numpy(gb).to(dev), int(gb[0])))
     B_mean = float(np.mean([q.shape[0] for q, _ in plan[W:]]))
 
+    pg = dist.group.WORLD if world > 1 else None
     params = wj.init_params(A, L, hidden=64, dropout=0.1, seed=11, device=dev)
     state = wj.AdamState.for_params(params, lr=1e-3)
-    step = wj.TrainStep(store, params, state, dense_dtype=torch.float32, mode=args.mode,
-                        use_graph=True, process_group=(dist.group.WORLD if world > 1 else None),
-                        seed=1000 + rank, overlap_inputs=True, launch=args.launch)
+    step = wj.TrainStep(store, params, state, dense_dtype=torch.float32, mode=args.mode, use_graph=True,
+                        process_group=pg, seed=1000 + rank, overlap_inputs=True, launch=args.launch)
     for k in range(W):                       # warm-up: captures every batch shape of the plan
         step(qd[k], yd[k], groups=gd[k])
     for k in range(W, W + K):
@@ -256,46 +467,35 @@ def run_ours(args, cfg):
         barrier_sync()
     t_step = max_over_ranks(e0.elapsed_time(e1) / 1e3 / K)
     final_loss = float(loss.item())
+    clk = clocks.summary()
 
-    # ---- join kernel alone, same batches, events on its stream
+    # ---- join kernel alone (dense fp32 tile), same batches
     dense_buf = {}
     j0, j1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    for k in range(W, W + K):  # warm
-        shp = qd[k].shape[0]
-        dense_buf.setdefault(shp, torch.empty((shp, A * M * (L + 1), A * (L + 1)), device=dev))
-        dense_batch(store, qd[k], out=dense_buf[shp], validate=False)
-    torch.cuda.synchronize()
-    j0.record()
-    for k in range(W, W + K):
-        dense_batch(store, qd[k], out=dense_buf[qd[k].shape[0]], validate=False)
-    j1.record()
-    torch.cuda.synchronize()
-    t_join = j0.elapsed_time(j1) / 1e3 / K
-    # ---- fused join+encode kernel alone (training: dropout + backward statistics)
-    enc_bufs = {}
-    step_t = torch.zeros(1, dtype=torch.int64, device=dev)
-    for k in range(W, W + K):
-        shp = qd[k].shape[0]
-        enc_bufs.setdefault(shp, {"pooled": torch.empty((shp, 64), device=dev),
-                                  "S": torch.empty((shp, A * (L + 1), 64), device=dev),
-                                  "msum": torch.empty((shp, 64), device=dev)})
-    t_enc = None
-    if A * (L + 1) <= 16:
-        def enc_launch(k):
-            if step.launch == "chain":  # the production kernel: dynamic scheduling over query groups
-                step.encode_only(qd[k], groups=gd[k])
-                return
-            b = enc_bufs[qd[k].shape[0]]
-            t = params.tensors
-            wj.encoder.join_encode(store, qd[k], t["w1"], t["b1"], 0.9, 5, step_t, b["pooled"], b["S"],
-                                   b["msum"])
-
-        for k in range(W, W + K):
-            enc_launch(k)
+    t_join = None
+    if M * (L + 1) * A * A * (L + 1) * 4 * B_mean < 8e9:
+        for k in range(W, W + K):  # warm
+            shp = qd[k].shape[0]
+            dense_buf.setdefault(shp, torch.empty((shp, A * M * (L + 1), A * (L + 1)), device=dev))
+            dense_batch(store, qd[k], out=dense_buf[shp], validate=False)
         torch.cuda.synchronize()
         j0.record()
         for k in range(W, W + K):
-            enc_launch(k)
+            dense_batch(store, qd[k], out=dense_buf[qd[k].shape[0]], validate=False)
+        j1.record()
+        torch.cuda.synchronize()
+        t_join = j0.elapsed_time(j1) / 1e3 / K
+        del dense_buf
+    # ---- fused join+encode kernel alone: the step's own kernel (dynamic
+    # scheduling over query groups), K launches between events on its stream
+    t_enc = None
+    if step.launch == "chain":
+        for k in range(W, W + K):
+            step.encode_only(qd[k], groups=gd[k])
+        torch.cuda.synchronize()
+        j0.record()
+        for k in range(W, W + K):
+            step.encode_only(qd[k], groups=gd[k])
         j1.record()
         torch.cuda.synchronize()
         t_enc = j0.elapsed_time(j1) / 1e3 / K
@@ -306,21 +506,20 @@ def run_ours(args, cfg):
     # batches come from the native planner (the reference's BFS batches +
     # in-seed negatives on numpy's PCG64 stream, pipeline.py:287-305) on its
     # producer thread: planning, H2D, step and the loss read-back are all
-    # inside the timed region.
+    # inside the timed region.  One full epoch (or K steps with --no-epoch).
     from paper_2202_13538_b200.pipeline import BatchPlanner, DeviceFeeder, TrainConfig
 
-    host_g = g.to_host()
-    nn_ = cfg["n"]
-    filt_rows = np.stack([split.all_edges // nn_, split.all_edges % nn_], 1)
+    host_g = wl.walk_graph.to_host()
     torch.cuda.synchronize()
     del store
     step = None
     barrier_sync()
     w0 = time.perf_counter()
     e0.record()
-    planner = BatchPlanner(split.train_pos, filt_rows, nn_, TrainConfig(batch_size=POS_PER_BATCH, k_neg=K_NEG),
+    planner = BatchPlanner(wl.train_pos, wl.filter_rows, wl.n,
+                           TrainConfig(batch_size=POS_PER_BATCH, k_neg=cfg["k_neg"]),
                            np.random.default_rng(BATCH_SEED + rank), depth=8, background=True)
-    store = prep(host_g, M, L, STORE_SEED)
+    store = wl.prep(host_g, sharded=world > 1 and args.pre == "sharded" and wl.edge_types is None)
     e1.record()
     torch.cuda.synchronize()
     t_pre_dev = e0.elapsed_time(e1) / 1e3
@@ -329,13 +528,12 @@ def run_ours(args, cfg):
     t_plan_setup = time.perf_counter() - w0  # the planner build, from the same start
     barrier_sync()
     t_pre_e2e = max_over_ranks(max(t_pre_dev, t_pre_wall_dev, t_plan_setup))
-    del filt_rows
     params = wj.init_params(A, L, hidden=64, dropout=0.1, seed=11, device=dev)
     state = wj.AdamState.for_params(params, lr=1e-3)
-    step = wj.TrainStep(store, params, state, dense_dtype=torch.float32, mode=args.mode,
-                        use_graph=True, process_group=(dist.group.WORLD if world > 1 else None),
-                        seed=1000 + rank, overlap_inputs=True, launch=args.launch)
-    loss_h = torch.empty(W + K, dtype=torch.float32).pin_memory()
+    step = wj.TrainStep(store, params, state, dense_dtype=torch.float32, mode=args.mode, use_graph=True,
+                        process_group=pg, seed=1000 + rank, overlap_inputs=True, launch=args.launch)
+    n_e2e = K if args.no_epoch else nb_epoch // world
+    loss_h = torch.empty(W + max(n_e2e, 1), dtype=torch.float32).pin_memory()
     chain = step.launch == "chain"
     # chain: pinned batch -> side-stream H2D into a device ring (one batch
     # ahead, completion checked on the host) -> step; the Adam kernel writes
@@ -358,26 +556,31 @@ def run_ours(args, cfg):
         e2e_step(k, q, y)
     it.close()
     barrier_sync()
-    h2d_list = []
+    h2d_total, steps_done = 0, 0
     w0 = time.perf_counter()
     e0.record()
     it = source()  # the producer thread starts inside the timed region
-    for k in range(W, W + K):
+    for k in range(W, W + n_e2e):
         try:
             q, y, _ = next(it)
-        except StopIteration:  # small graphs: the epoch ends, the next one starts (as in train())
+        except StopIteration:  # small graphs / short epochs: the next epoch starts (as in train())
             it = source()
             q, y, _ = next(it)
         e2e_step(k, q, y)
-        h2d_list.append(q.numel() * 8 + (0 if chain else y.numel() * 4))
+        h2d_total += q.numel() * 8 + (0 if chain else y.numel() * 4)
+        steps_done += 1
     e1.record()
     barrier_sync()
-    wall = (time.perf_counter() - w0) / K
+    wall = time.perf_counter() - w0
     it.close()
     planner.close()
-    t_dev_e2e = e0.elapsed_time(e1) / 1e3 / K
-    t_step_e2e = max_over_ranks(max(t_dev_e2e, wall))
-    h2d = int(np.mean(h2d_list))
+    t_dev_e2e = e0.elapsed_time(e1) / 1e3
+    t_run_e2e = max_over_ranks(max(t_dev_e2e, wall))
+    h2d = int(h2d_total / max(steps_done, 1))
+    if args.no_epoch:
+        e2e = q_epoch / (t_pre_e2e + (nb_epoch / world) * t_run_e2e / max(steps_done, 1))
+    else:
+        e2e = q_epoch / (t_pre_e2e + t_run_e2e)
 
     if args.mode == "fused" and step.fast_tail:
         launches_per_step = 3
@@ -389,70 +592,11 @@ def run_ours(args, cfg):
         launches_per_step = 1
         launches_note = "per timed step: wj_join (the encoder runs as PyTorch/cuBLAS kernels)"
     value = q_epoch / (t_pre + (nb_epoch / world) * t_step)
-    e2e = q_epoch / (t_pre_e2e + (nb_epoch / world) * t_step_e2e)
 
-    # ---- roofline of the join kernel (SURVEY §8(d) join bytes per query)
+    # ---- roofline of the dominant kernel
     hbm, peak_kind = peaks()
-    s_bytes = 4  # fp32 dense elements
-    c = 1 if M <= 255 else 2
-    join_bytes_q = A * M * (L + 1) * 4 + A * ubar * (4 + c * (L + 1)) + A * A * M * (L + 1) ** 2 * s_bytes
-    achieved = join_bytes_q * B_mean / t_join / 1e9
-    # whole-step bytes per query (B_q of SURVEY §8(d), dense at s=4)
-    b_pre = M * L * 64 + 2 * M * (L + 1) * 4 + ubar * (4 + c * (L + 1))
-    b_q = (A * M * (L + 1) * 4 + A * ubar * (4 + c * (L + 1)) + 3 * A * A * M * (L + 1) ** 2 * s_bytes
-           + b_pre * cfg["n"] / q_epoch)
-    # fused kernel: what it must move per query -- the A anchors' sorted
-    # (uniq_x, uniq_id) lists in, pooled/msum/S out (the dense tile and the
-    # [rows, 64] activations never exist)
-    AW = A * (L + 1)
-    vbar = (store.vslots_d.numel() - 2) / store.num_nodes if store.vslots_d is not None else 0.0
-    # per query: query ids + per-anchor offsets / vindex entries, the anchors'
-    # sorted (uniq_x, uniq_id) lists, their virtual-landing lists (uint16);
-    # written: pooled, msum and S (fp32)
-    enc_bytes_q = A * (8 + 16 + 16) + A * ubar * 8 + A * vbar * 2 + (2 + AW) * 64 * 4
-    kname = "wj_join_encode" if args.mode == "fused" else "wj_join"
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", f"{args.config}_{kname}_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get("bytes_per_launch")
-        except Exception:
-            traffic = None
-    if args.mode == "fused" and t_enc:
-        # achieved = SURVEY 8(d)'s per-query join figure (walk blocks + the
-        # anchors' RPE index + the dense tile at s = 2 B: 57.5 KB at C3) x the
-        # launch's queries / the launch time.  The fused kernel does that
-        # join's work without materialising the tile; the bytes it must move
-        # itself (enc_bytes_q) are reported beside it as "minimal".
-        sv_bytes_q = A * M * (L + 1) * 4 + A * ubar * (4 + c * (L + 1)) + A * A * M * (L + 1) ** 2 * 2
-        ach = sv_bytes_q * B_mean / t_enc / 1e9
-        roof = {"kernel": "wj_join_encode (join + densify + layer-1 fwd/bwd statistics)", "bound": "hbm",
-                "achieved": round(ach, 1), "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
-                "frac": round(ach / hbm, 4), "traffic": traffic,
-                "bytes_per_query": round(sv_bytes_q, 1),
-                "bytes_definition": "SURVEY 8(d) join bytes per query (A*M*(L+1)*4 + A*Ubar*(4+c*(L+1)) + "
-                                    "A^2*M*(L+1)^2*2) x queries per launch",
-                "kernel_ms": round(t_enc * 1e3, 4), "kernel_share_of_step": round(t_enc / t_step, 3),
-                "minimal": {"bytes_per_query": round(enc_bytes_q, 1),
-                            "achieved": round(enc_bytes_q * B_mean / t_enc / 1e9, 1),
-                            "frac": round(enc_bytes_q * B_mean / t_enc / 1e9 / hbm, 4),
-                            "definition": "bytes the fused kernel must move: anchor lists + virtual-landing "
-                                          "lists + metadata in, pooled/msum/S out"},
-                "note": ("not HBM-bound: issue-bound on the integer ALU (dropout hash) and latency-bound in "
-                         "the per-query prepass (ncu: ALU pipe ~53%, DRAM <1%); see DESIGN.md"),
-                "traffic_note": "ncu dram bytes of one launch (profiles/c3_wj_join_encode_traffic.json)"}
-    else:
-        roof = {"kernel": "wj_join (join + densify, fp32 dense)", "bound": "hbm",
-                "achieved": round(achieved, 1), "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
-                "frac": round(achieved / hbm, 4), "traffic": traffic,
-                "bytes_per_query": round(join_bytes_q, 1), "kernel_ms": round(t_join * 1e3, 4),
-                "kernel_share_of_step": round(t_join / t_step, 3)}
-    roof["wj_join_dense_fp32"] = {"achieved_gbs": round(achieved, 1), "frac": round(achieved / hbm, 4),
-                                  "ms": round(t_join * 1e3, 4), "bytes_per_query": round(join_bytes_q, 1)}
-    roof["north_star"] = {"bytes_per_query_B_q": round(b_q, 1),
-                          "frac": round(b_q * B_mean / t_step / 1e9 / hbm, 4),
-                          "definition": "SURVEY 8(d) B_q * step queries / t_step / peak (40% target)"}
-
+    roof = roofline_train(cfg, args, ubar, B_mean, t_enc, t_join, t_step, hbm, peak_kind, clk,
+                          store.num_nodes, q_epoch)
     out = {
         "metric": METRIC,
         "value": round(value, 1),
@@ -465,41 +609,182 @@ def run_ours(args, cfg):
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "int32 walk/RPE/join, fp32 encoder",
-        "data": "synthetic (Erdos-Renyi graph of the named shape, random-init encoder)",
-        "config": {
-            "workload": f"{cfg['workload']} ER n={cfg['n']} m={cfg['m']}, M={M}, L={L}, A={A}, "
-                        f"5% link split, batches of {POS_PER_BATCH} pos + {K_NEG}/pos neg",
-            "n_nodes": cfg["n"], "n_edges": cfg["m"], "walk_graph_edges": int(g.indices.numel() // 2),
-            "M": M, "L": L, "arity": A, "queries_per_step": B_mean,
-            "train_pos": int(split.train_pos.shape[0]), "Q_epoch": q_epoch,
-            "batches_per_epoch": nb_epoch, "t_pre_ms": round(t_pre * 1e3, 3),
-            "t_pre_phase_ms": {k: round(v, 3) for k, v in phase_ms.items()},
-            "store_entries": int(store.num_entries), "ubar_measured": round(ubar, 2),
-            "table_size": int(store.table_keys_d.numel()),
+        "data": "synthetic (graph of the named shape, random-init encoder)",
+        "config": _common_config(cfg, wl, store, ctx, {
+            "queries_per_step": B_mean, "train_pos": int(wl.train_pos.shape[0]), "k_neg": cfg["k_neg"],
+            "Q_epoch": q_epoch, "batches_per_epoch": nb_epoch,
             "value_formula": "Q_epoch / (t_pre + batches_per_epoch / n_gpus * t_step)",
-            "l2": "inputs larger than L2 (store > 40 GB, a different random batch every step)",
-            "final_loss": final_loss,
-            "parallelism": f"dp{world}",
-            "launch": step.launch,
-            "preprocess": args.pre if world > 1 else "single",
-        },
+            "final_loss": final_loss, "parallelism": f"dp{world}", "launch": args.launch,
+            "preprocess": args.pre if world > 1 else "single"}),
         "e2e": {"value": round(e2e, 1), "unit": "queries/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": 4, "t_pre_ms": round(t_pre_e2e * 1e3, 3),
                 "t_planner_setup_ms": round(t_plan_setup * 1e3, 3),
                 "t_pre_note": "device preprocess and the planner build (host thread) overlap; t_pre is the later end",
-                "device_ms_per_step": round(t_dev_e2e * 1e3, 4), "wall_ms_per_step": round(wall * 1e3, 4),
-                "ms_per_step": round(t_step_e2e * 1e3, 4),
+                "steps_timed": steps_done, "full_epoch": not args.no_epoch,
+                "t_run_s": round(t_run_e2e, 4), "device_s": round(t_dev_e2e, 4), "wall_s": round(wall, 4),
+                "ms_per_step": round(t_run_e2e / max(steps_done, 1) * 1e3, 4),
+                "formula": ("Q_epoch / (t_pre + t_epoch): every batch of one full epoch timed"
+                            if not args.no_epoch else "Q_epoch / (t_pre + batches_per_epoch * t_step)"),
                 "path": ("host CSR -> preprocess; native batch planner (producer thread) -> pinned batch "
                          "-> H2D (side stream, one batch ahead) -> step (chain executor) -> loss D2H "
                          "(written into pinned memory by the Adam kernel), every step timed")},
         "roofline": roof,
         "gpu_launches": K * launches_per_step,
         "gpu_launches_note": launches_note,
-        "clocks": clocks.summary(),
+        "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(args, cfg, split, index, filt, plan[W], q_epoch, nb_epoch,
-                                           g)
+        out["cpu_baseline"] = cpu_baseline(args, cfg, wl, plan[W], q_epoch, nb_epoch)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def roofline_train(cfg, args, ubar, B_mean, t_enc, t_join, t_step, hbm, peak_kind, clk, n, q_epoch):
+    """roofline.* of the train bench: the fused kernel's achieved bytes per
+    launch (SURVEY §8(d) join bytes at s = 2) / its live launch time, its
+    issue-slot fraction from the committed ncu capture's instruction count,
+    and BASELINE.md's whole-step north-star fraction."""
+    import torch
+
+    M, L, A = cfg["M"], cfg["L"], cfg["A"]
+    cfg_name = [k for k, v in CONFIGS.items() if v is cfg][0]
+    jb2 = join_bytes_q(cfg, ubar, 2)
+    b_q = b_q_baseline(cfg, ubar, n, q_epoch)
+    ns = {"bytes_per_query_B_q": round(b_q, 1), "s_bytes": 2,
+          "frac": round(b_q * B_mean / t_step / 1e9 / hbm, 4),
+          "definition": "BASELINE.md §2 B_q (dense tile at s = 2 B) * step queries / t_step / peak; target 0.40"}
+    if args.mode == "fused" and t_enc:
+        ncu, fresh = ncu_capture(cfg_name, "wj_join_encode")
+        ach = jb2 * B_mean / t_enc / 1e9
+        roof = {"kernel": "wj_join_encode (join + densify + layer-1 fwd/bwd statistics)", "bound": "hbm",
+                "achieved": round(ach, 1), "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
+                "frac": round(ach / hbm, 4),
+                "traffic": (ncu or {}).get("dram_bytes_per_launch"),
+                "traffic_source": (f"profiles/{cfg_name}_wj_join_encode_ncu.json (ncu --set full of one launch; "
+                                   f"same sources: {fresh})") if ncu else None,
+                "bytes_per_query": round(jb2, 1), "queries_per_launch": B_mean,
+                "bytes_definition": "SURVEY 8(d) join bytes per query (A*M*(L+1)*4 + A*Ubar*(4+c*(L+1)) + "
+                                    "A^2*M*(L+1)^2*2) x queries per launch / live launch time",
+                "kernel_ms": round(t_enc * 1e3, 4), "kernel_share_of_step": round(t_enc / t_step, 3),
+                "note": ("not HBM-bound: the batch's ~48 anchors' lists stay in L2 (DRAM traffic ~0.4 MB per "
+                         "launch); the kernel is issue- and latency-bound (dropout hash on the integer ALU, "
+                         "latency-bound per-unit prepass) -- see issue_roof and DESIGN.md")}
+        if ncu and ncu.get("inst_executed"):
+            sm_mhz = clk.get("sm_mhz") or ncu.get("sm_mhz") or 1965.0
+            issue_cap = 4 * torch.cuda.get_device_properties(0).multi_processor_count * sm_mhz * 1e6 * t_enc  # warp-instructions the SMs could issue
+            roof["issue_roof"] = {
+                "warp_instructions_per_launch": ncu["inst_executed"],
+                "frac": round(ncu["inst_executed"] / issue_cap, 4),
+                "definition": "ncu smsp__inst_executed.sum of one launch / (4 schedulers x SMs x SM clock x "
+                              "live launch time)",
+                "ncu_issue_slots_busy": ncu.get("issue_slots_busy_pct"),
+                "alu_pipe_pct": ncu.get("alu_pipe_pct"), "same_sources": fresh}
+    else:
+        jb4 = join_bytes_q(cfg, ubar, 4)
+        ach = jb4 * B_mean / t_join / 1e9
+        roof = {"kernel": "wj_join (join + densify, fp32 dense)", "bound": "hbm",
+                "achieved": round(ach, 1), "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
+                "frac": round(ach / hbm, 4), "traffic": None, "bytes_per_query": round(jb4, 1),
+                "kernel_ms": round(t_join * 1e3, 4), "kernel_share_of_step": round(t_join / t_step, 3)}
+    if t_join:
+        jb4 = join_bytes_q(cfg, ubar, 4)
+        roof["wj_join_dense_fp32"] = {"achieved_gbs": round(jb4 * B_mean / t_join / 1e9, 1),
+                                      "frac": round(jb4 * B_mean / t_join / 1e9 / hbm, 4),
+                                      "ms": round(t_join * 1e3, 4), "bytes_per_query": round(jb4, 1)}
+    roof["north_star"] = ns
+    return roof
+
+
+def run_ours_infer(args, cfg, store, ctx):
+    """Scoring throughput (pipeline.py:185-198,329-355 on the device)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2202_13538_b200 as wj
+    from paper_2202_13538_b200 import encoder as E
+
+    world, rank, local, dev = ctx["world"], ctx["rank"], ctx["local"], ctx["dev"]
+    barrier_sync, max_over_ranks = ctx["barrier_sync"], ctx["max_over_ranks"]
+    wl, ubar = ctx["wl"], ctx["ubar"]
+    A, L = cfg["A"], cfg["L"]
+    W, K = args.warmup, args.steps
+    chunks = infer_queries(wl, W + K, BATCH_SEED + 100 + rank)
+    B = chunks[0].shape[0]
+    qd = [torch.from_numpy(c).to(dev) for c in chunks]
+    params = wj.init_params(A, L, hidden=64, dropout=0.1, seed=11, device=dev)
+    scorer = E.FusedScorer(params, store)
+    for k in range(W):
+        scorer.logits(qd[k])
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local, enabled=not args.no_clocks) as clocks:
+        barrier_sync()
+        torch.cuda._sleep(2_000_000)
+        e0.record()
+        for k in range(W, W + K):
+            logits = scorer.logits(qd[k])
+        e1.record()
+        barrier_sync()
+    t_step = max_over_ranks(e0.elapsed_time(e1) / 1e3 / K)
+    clk = clocks.summary()
+    # the join+encode kernel alone (keep = 1 variant)
+    pooled = torch.empty((B, 64), device=dev)
+    t = params.tensors
+    for k in range(W):
+        E.join_encode(store, qd[k], t["w1"], t["b1"], 1.0, 0, None, pooled)
+    torch.cuda.synchronize()
+    e0.record()
+    for k in range(W, W + K):
+        E.join_encode(store, qd[k], t["w1"], t["b1"], 1.0, 0, None, pooled)
+    e1.record()
+    torch.cuda.synchronize()
+    t_enc = e0.elapsed_time(e1) / 1e3 / K
+    # e2e through the public API: pinned host queries -> score_array -> scores to host
+    pinned = [torch.from_numpy(c).pin_memory() for c in chunks]
+    for k in range(W):
+        wj.score_array(store, params, pinned[k]).cpu()
+    barrier_sync()
+    w0 = time.perf_counter()
+    for k in range(W, W + K):
+        s = wj.score_array(store, params, pinned[k]).cpu()
+    barrier_sync()
+    t_e2e = max_over_ranks((time.perf_counter() - w0) / K)
+    value = B * world / t_step
+    e2e = B * world / t_e2e
+    hbm, peak_kind = peaks()
+    jb2 = join_bytes_q(cfg, ubar, 2)
+    ach = jb2 * B / t_enc / 1e9
+    cfg_name = [k for k, v in CONFIGS.items() if v is cfg][0]
+    ncu, fresh = ncu_capture(cfg_name, "wj_join_encode_infer")
+    out = {
+        "metric": METRIC_INFER, "value": round(value, 1), "unit": "queries/s", "n_gpus": world, "steps": K,
+        "warmup": W, "ms_per_step": round(t_step * 1e3, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int32 join, fp32 encoder (no dropout)",
+        "data": "synthetic (graph of the named shape, random-init encoder)",
+        "config": _common_config(cfg, wl, store, ctx, {
+            "queries_per_step": B, "protocol": f"{INFER_POS_PER_STEP} positives x (1 + "
+                                              f"{cfg.get('infer_neg', INFER_NEG)} negatives sharing the "
+                                              f"positive's first {A - 1} node(s)) per step (PAPER.md:284)",
+            "parallelism": f"dp{world} (independent query chunks)"}),
+        "e2e": {"value": round(e2e, 1), "unit": "queries/s", "h2d_bytes_per_step": int(B * A * 8),
+                "d2h_bytes_per_step": int(B * 8), "ms_per_step": round(t_e2e * 1e3, 4),
+                "path": "pinned host queries -> score_array (range check, H2D, join+encode keep=1, logits tail, "
+                        "sigmoid) -> float64 scores to host, every step timed (wall clock, synchronised)"},
+        "roofline": {"kernel": "wj_join_encode keep = 1 variant (join + densify + layer 1, distinct landings)",
+                     "bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "peak_kind": peak_kind,
+                     "unit": "GB/s", "frac": round(ach / hbm, 4),
+                     "traffic": (ncu or {}).get("dram_bytes_per_launch"),
+                     "traffic_source": (f"profiles/{cfg_name}_wj_join_encode_infer_ncu.json (same sources: "
+                                        f"{fresh})") if ncu else None,
+                     "bytes_per_query": round(jb2, 1), "queries_per_launch": B,
+                     "kernel_ms": round(t_enc * 1e3, 4), "kernel_share_of_step": round(t_enc / t_step, 3)},
+        "gpu_launches": 2 * K,
+        "gpu_launches_note": "per timed step: wj_join_encode (keep = 1 variant) + wj_encoder_tail (logits)",
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline_infer(cfg, wl, chunks[W])
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
@@ -512,7 +797,7 @@ def cpu_reference_batch(cfg, idxptr, indices, q, y, index_ref, pos_ref, filt_ref
                         threads, params, adam, drop_rng):
     """One reference training-loop body on the host (pipeline.py:293-310),
     timed without the untimed sub-store build.  Returns (seconds, parts)."""
-    from oracle import core, pipeline_ref
+    from oracle import core, encoder_ref, pipeline_ref
 
     M, L = cfg["M"], cfg["L"]
     # sub-store over the batch's anchors (preprocess work -- accounted in t_pre)
@@ -522,10 +807,8 @@ def cpu_reference_batch(cfg, idxptr, indices, q, y, index_ref, pos_ref, filt_ref
     ql = local.reshape(q.shape).astype(np.int64)
     parts = {}
     t0 = time.perf_counter()
-    pipeline_ref.make_batch(index_ref, pos_ref, filt_ref, rng_ref)  # BFS + negatives (exact ref)
+    pipeline_ref.make_batch(index_ref, pos_ref, filt_ref, rng_ref, k_neg=cfg["k_neg"])  # BFS + negatives (exact ref)
     t1 = time.perf_counter()
-    from oracle import encoder_ref
-
     dense = core.dense_batch(sub, ql, threads)
     t2 = time.perf_counter()
     logits, cache = encoder_ref.forward(params, dense, L, dropout=0.1, training=True, dropout_rng=drop_rng)
@@ -539,24 +822,31 @@ def cpu_reference_batch(cfg, idxptr, indices, q, y, index_ref, pos_ref, filt_ref
 
 class _FastFilter(set):
     """Set-like positive filter over sorted packed keys for the reference
-    negative sampler (membership only; same answers as the reference set)."""
+    negative sampler (membership of canonical tuples; same answers as the
+    reference set)."""
 
-    def __init__(self, keys, n):
+    def __init__(self, rows, n):
         super().__init__()
-        self.keys, self.n = keys, n
+        t = np.sort(np.asarray(rows, dtype=np.int64), axis=1)
+        k = np.zeros(t.shape[0], dtype=np.int64)
+        for c in range(t.shape[1]):
+            k = k * n + t[:, c]
+        self.keys, self.n = np.unique(k), n
 
     def __contains__(self, t):
-        k = int(t[0]) * self.n + int(t[1])
+        k = 0
+        for v in t:
+            k = k * self.n + int(v)
         i = np.searchsorted(self.keys, k)
         return bool(i < len(self.keys) and self.keys[i] == k)
 
 
-def cpu_setup(cfg, split, index_q_limit=None):
+def cpu_setup(wl):
     from oracle import pipeline_ref
 
-    pos = [tuple(r) for r in split.train_pos.tolist()]
+    pos = [tuple(r) for r in wl.train_pos.tolist()]
     index_ref = pipeline_ref.QueryOverlapIndex(pos)
-    filt_ref = _FastFilter(split.all_edges, cfg["n"])
+    filt_ref = _FastFilter(wl.filter_rows, wl.n)
     return pos, index_ref, filt_ref
 
 
@@ -565,27 +855,31 @@ def cpu_preprocess_shard(cfg, idxptr, indices, shard, threads):
     from oracle import core
 
     M, L = cfg["M"], cfg["L"]
-    nodes = np.arange(shard, dtype=np.int64)
+    n = idxptr.shape[0] - 1
+    nodes = np.arange(min(shard, n), dtype=np.int64)
     t0 = time.perf_counter()
     walks = core.sample_nodes(idxptr, indices, nodes, M, L, STORE_SEED, threads)
     t_sample = time.perf_counter() - t0
     st = core.store_from_walks(walks, STORE_SEED, threads, timed=True)
     ph = dict(st.phase_seconds, sample=t_sample)
-    scale = cfg["n"] / shard
+    scale = n / nodes.shape[0]
     return sum(ph.values()) * scale, {k: round(v * scale, 3) for k, v in ph.items()}
 
 
-def cpu_baseline(args, cfg, split, index, filt, batch, q_epoch, nb_epoch, g, budget_s=30.0):
+def _host_csr(wl):
+    host = wl.walk_graph.to_host()
+    return np.ascontiguousarray(host.idxptr, np.int64), np.ascontiguousarray(host.indices, np.int32)
+
+
+def cpu_baseline(args, cfg, wl, batch, q_epoch, nb_epoch):
     """Oracle (port of the reference CPU path) on this host's cores, bounded sample."""
     from oracle import core, encoder_ref
 
     threads = core.default_threads()
-    host = g.to_host()
-    idxptr = np.ascontiguousarray(host.idxptr, np.int64)
-    indices = np.ascontiguousarray(host.indices, np.int32)
-    shard = args.cpu_shard_nodes or min(cfg["n"], max(2000, 5000 * threads // 8))
+    idxptr, indices = _host_csr(wl)
+    shard = args.cpu_shard_nodes or min(wl.n, max(2000, 5000 * threads // 8))
     t_pre, ph = cpu_preprocess_shard(cfg, idxptr, indices, shard, threads)
-    pos, index_ref, filt_ref = cpu_setup(cfg, split)
+    pos, index_ref, filt_ref = cpu_setup(wl)
     q, y = batch
     params = encoder_ref.init_params(cfg["A"], cfg["L"], seed=11)
     adam = encoder_ref.Adam(params)
@@ -598,14 +892,44 @@ def cpu_baseline(args, cfg, split, index, filt, batch, q_epoch, nb_epoch, g, bud
     per_q = (t_sub - parts["batchgen"]) / sub
     t_batch = parts["batchgen"] + per_q * q.shape[0]
     value = q_epoch / (t_pre + nb_epoch * t_batch)
+    typed = " (untyped sampler as the cost proxy: the reference has no typed sampler)" if wl.edge_types is not None \
+        else ""
     return {"value": round(value, 3), "unit": "queries/s", "cores": threads, "kind": "port",
-            "sample": f"preprocess on nodes [0,{shard}) scaled x{cfg['n'] / shard:.1f} "
+            "sample": f"preprocess on nodes [0,{shard}) scaled x{wl.n / min(shard, wl.n):.1f}{typed} "
                       f"(sequential intern scaled linearly, estimated); one batch's join+densify+"
                       f"fp64 encoder fwd/bwd/Adam on {sub} of {q.shape[0]} queries scaled linearly, "
                       f"plus the exact reference BFS batch generation",
             "t_pre_s": round(t_pre, 3), "t_pre_phase_s": ph, "t_batch_s": round(t_batch, 4),
             "batch_parts_s": {k: round(v, 4) for k, v in parts.items()},
             "cpu": _cpu_model()}
+
+
+def cpu_infer_chunk(cfg, idxptr, indices, q, threads, params):
+    """The reference scoring path on one chunk (pipeline.py:185-198): dense
+    join + float64 forward, sub-store of the chunk's anchors built untimed."""
+    from oracle import core, encoder_ref
+
+    anchors, local = np.unique(q, return_inverse=True)
+    walks = core.sample_nodes(idxptr, indices, anchors, cfg["M"], cfg["L"], STORE_SEED, threads)
+    sub = core.store_from_walks(walks, STORE_SEED, threads)
+    ql = local.reshape(q.shape).astype(np.int64)
+    t0 = time.perf_counter()
+    dense = core.dense_batch(sub, ql, threads)
+    encoder_ref.forward(params, dense, cfg["L"], training=False)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline_infer(cfg, wl, chunk, sample=1001):
+    from oracle import core, encoder_ref
+
+    threads = core.default_threads()
+    idxptr, indices = _host_csr(wl)
+    params = encoder_ref.init_params(cfg["A"], cfg["L"], seed=11)
+    q = chunk[:sample]
+    t = cpu_infer_chunk(cfg, idxptr, indices, q, threads, params)
+    return {"value": round(q.shape[0] / t, 3), "unit": "queries/s", "cores": threads, "kind": "port",
+            "sample": f"{q.shape[0]} queries (one positive + its negatives) of the first timed chunk: oracle "
+                      f"join + densify + float64 encoder forward", "cpu": _cpu_model()}
 
 
 def _cpu_model():
@@ -628,18 +952,41 @@ def run_reference(args, cfg):
     from oracle import core, encoder_ref
 
     dev = torch.device("cuda", local) if torch.cuda.is_available() else torch.device("cpu")
-    split, index, filt = build_inputs(cfg, dev)
-    q_epoch, nb_epoch = epoch_shape(split)
-    g = split.walk_graph
+    wl = build_workload(cfg, dev)
     threads = core.default_threads()
-    host = g.to_host()
-    idxptr = np.ascontiguousarray(host.idxptr, np.int64)
-    indices = np.ascontiguousarray(host.indices, np.int32)
-    shard = args.cpu_shard_nodes or min(cfg["n"], max(2000, 5000 * threads // 8))
-    t_pre, ph = cpu_preprocess_shard(cfg, idxptr, indices, shard, threads)
-    pos, index_ref, filt_ref = cpu_setup(cfg, split)
+    idxptr, indices = _host_csr(wl)
     W, K = args.warmup, args.steps
-    plan = make_plan(split, index, filt, W + K, BATCH_SEED)
+    if args.what == "infer":
+        chunks = infer_queries(wl, W + K, BATCH_SEED + 100)
+        params = encoder_ref.init_params(cfg["A"], cfg["L"], seed=11)
+        sub = max(64, min(2002, int(2002 * 12 / max(W + K, 1))))
+        times = []
+        for k in range(W + K):
+            q = chunks[k][:sub]
+            t = cpu_infer_chunk(cfg, idxptr, indices, q, threads, params)
+            if k >= W:
+                times.append(t / q.shape[0])
+        value = 1.0 / float(np.mean(times))
+        out = {"metric": METRIC_INFER, "value": round(value, 3), "unit": "queries/s", "n_gpus": world, "steps": K,
+               "warmup": W, "ms_per_step": round(float(np.mean(times)) * chunks[0].shape[0] * 1e3, 3),
+               "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+               "dtype": "int64/int32 kernels, fp64 encoder", "data": "synthetic (same generator and seeds as the GPU arm)",
+               "impl": "reference",
+               "config": {"workload": f"{cfg['workload']} ({wl.desc}), M={cfg['M']}, L={cfg['L']}, A={cfg['A']}",
+                          "parallelism": "host threads"},
+               "cpu_baseline": {"value": round(value, 3), "unit": "queries/s", "cores": threads, "kind": "port",
+                                "sample": f"each step scores the first {sub} queries of its chunk (oracle join + "
+                                          f"densify + float64 forward), rate scaled to the chunk",
+                                "cpu": _cpu_model()},
+               "e2e": {"value": round(value, 3), "unit": "queries/s", "h2d_bytes_per_step": 0,
+                       "d2h_bytes_per_step": 0}}
+        print(json.dumps(out), flush=True)
+        return
+    q_epoch, nb_epoch = epoch_shape(wl)
+    shard = args.cpu_shard_nodes or min(wl.n, max(2000, 5000 * threads // 8))
+    t_pre, ph = cpu_preprocess_shard(cfg, idxptr, indices, shard, threads)
+    pos, index_ref, filt_ref = cpu_setup(wl)
+    plan = make_plan(wl, W + K, BATCH_SEED)
     params = encoder_ref.init_params(cfg["A"], cfg["L"], seed=11)
     adam = encoder_ref.Adam(params)
     rng_ref = np.random.default_rng(BATCH_SEED)
@@ -647,7 +994,7 @@ def run_reference(args, cfg):
     # per-step sample bounded so the whole --steps K --warmup W run stays
     # within about a minute of encoder time (the fp64 encoder is ~1.8 s per
     # 408 queries at C3): 408 queries for K + W <= 25, fewer beyond, >= 32
-    sub = 408 if cfg["n"] > 100_000 else 1632
+    sub = 408 if wl.n > 100_000 else 1632
     sub = max(32, min(sub, int(sub * 25 / max(W + K, 1))))
     times = []
     for k in range(W + K):
@@ -665,9 +1012,8 @@ def run_reference(args, cfg):
         "steps": K, "warmup": W, "ms_per_step": round(t_batch * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int64/int32 kernels, fp64 encoder",
         "data": "synthetic (same generator and seeds as the GPU arm)", "impl": "reference",
-        "config": {"workload": f"{cfg['workload']} ER n={cfg['n']} m={cfg['m']}, M={cfg['M']}, "
-                               f"L={cfg['L']}, A={cfg['A']}", "Q_epoch": q_epoch,
-                   "batches_per_epoch": nb_epoch, "t_pre_s_estimated": round(t_pre, 3),
+        "config": {"workload": f"{cfg['workload']} ({wl.desc}), M={cfg['M']}, L={cfg['L']}, A={cfg['A']}",
+                   "Q_epoch": q_epoch, "batches_per_epoch": nb_epoch, "t_pre_s_estimated": round(t_pre, 3),
                    "t_pre_phase_s": ph, "parallelism": "host threads"},
         "cpu_baseline": {"value": round(value, 3), "unit": "queries/s", "cores": threads, "kind": "port",
                          "sample": f"preprocess on nodes [0,{shard}) scaled to n; each step = reference "
