@@ -550,29 +550,41 @@ def run_ours_train(args, cfg, store, ctx):
             loss_h[k:k + 1].copy_(step(q, y).reshape(1), non_blocking=True)
             planner.release(step.input_event)
 
-    it = source()  # warm-up epoch: captures the step graphs, then abandoned
-    for k in range(W):
-        q, y, _ = next(it)
-        e2e_step(k, q, y)
-    it.close()
+    native = chain and world == 1  # the native epoch loop (wj_train_epoch): no Python between steps
+    if native:
+        step.run_epoch(planner, loss_out=loss_h, max_steps=W)  # warm-up, then abandoned
+    else:
+        it = source()  # warm-up epoch: captures the step graphs, then abandoned
+        for k in range(W):
+            q, y, _ = next(it)
+            e2e_step(k, q, y)
+        it.close()
     barrier_sync()
     h2d_total, steps_done = 0, 0
     w0 = time.perf_counter()
     e0.record()
-    it = source()  # the producer thread starts inside the timed region
-    for k in range(W, W + n_e2e):
-        try:
-            q, y, _ = next(it)
-        except StopIteration:  # small graphs / short epochs: the next epoch starts (as in train())
-            it = source()
-            q, y, _ = next(it)
-        e2e_step(k, q, y)
-        h2d_total += q.numel() * 8 + (0 if chain else y.numel() * 4)
-        steps_done += 1
+    if native:  # the producer thread starts inside the timed region
+        while steps_done < n_e2e:
+            k = step.run_epoch(planner, loss_out=loss_h[W + steps_done:], max_steps=n_e2e - steps_done)
+            if k == 0:
+                break
+            steps_done += k
+            h2d_total += step.last_epoch_h2d_bytes  # query ids + their query groups, counted natively
+    else:
+        it = source()  # the producer thread starts inside the timed region
+        for k in range(W, W + n_e2e):
+            try:
+                q, y, _ = next(it)
+            except StopIteration:  # small graphs / short epochs: the next epoch starts (as in train())
+                it = source()
+                q, y, _ = next(it)
+            e2e_step(k, q, y)
+            h2d_total += q.numel() * 8 + (0 if chain else y.numel() * 4)
+            steps_done += 1
+        it.close()
     e1.record()
     barrier_sync()
     wall = time.perf_counter() - w0
-    it.close()
     planner.close()
     t_dev_e2e = e0.elapsed_time(e1) / 1e3
     t_run_e2e = max_over_ranks(max(t_dev_e2e, wall))
@@ -626,8 +638,10 @@ def run_ours_train(args, cfg, store, ctx):
                 "formula": ("Q_epoch / (t_pre + t_epoch): every batch of one full epoch timed"
                             if not args.no_epoch else "Q_epoch / (t_pre + batches_per_epoch * t_step)"),
                 "path": ("host CSR -> preprocess; native batch planner (producer thread) -> pinned batch "
-                         "-> H2D (side stream, one batch ahead) -> step (chain executor) -> loss D2H "
-                         "(written into pinned memory by the Adam kernel), every step timed")},
+                         "-> H2D (copy stream, one batch ahead) -> step (chain executor) -> loss D2H "
+                         "(written into pinned memory by the Adam kernel), every step timed; "
+                         + ("native epoch loop (TrainStep.run_epoch / wj_train_epoch)" if native else
+                            "Python loop (DeviceFeeder + TrainStep)"))},
         "roofline": roof,
         "gpu_launches": K * launches_per_step,
         "gpu_launches_note": launches_note,

@@ -372,6 +372,23 @@ int wj_planner_acquire(wj_planner *planner, int32_t *slot_out, int64_t *n_querie
 int wj_planner_release(wj_planner *planner, int32_t slot);
 int wj_planner_stop(wj_planner *planner);
 
+/* ---- Native training epoch (replaces train()'s batch loop body,
+ * pipeline.py:287-310, when planner and step executor are native) ----------
+ * After wj_planner_start_epoch on the pinned ring (ring_q [n_slots, cap,
+ * arity], ring_g [n_slots, (2+arity)*cap + 2]): for every batch of the epoch
+ * (or the first max_steps; max_steps < 0: all), copy it H2D on copy_stream
+ * one batch ahead into a device ring (dev_q [dev_depth, cap, arity], dev_g
+ * [dev_depth, (2+arity)*cap + 2]), then wj_stepper_run on stream with labels
+ * dev_labels + cap - n_pos (dev_labels = cap ones then cap zeros) and the
+ * loss into loss_out[k] (device or pinned host).  Planner slots are handed
+ * back once copied; steps_done receives the number of steps launched and
+ * h2d_bytes (nullable) the bytes copied host -> device (batches issued).  The
+ * caller stops the planner if max_steps ended the loop before the epoch. */
+int wj_train_epoch(wj_stepper *stepper, wj_planner *planner, const int64_t *ring_q, const int32_t *ring_g,
+                   int32_t n_slots, int64_t cap, int32_t arity, int64_t *dev_q, int32_t *dev_g, int32_t dev_depth,
+                   const float *dev_labels, float *loss_out, int64_t max_steps, wj_stream_t stream,
+                   wj_stream_t copy_stream, int64_t *steps_done, int64_t *h2d_bytes);
+
 #ifdef __cplusplus
 }
 #endif

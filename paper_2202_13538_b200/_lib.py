@@ -68,6 +68,7 @@ SIGNATURES = {
     "wj_planner_acquire": [P, P, P, P],
     "wj_planner_release": [P, I32],
     "wj_planner_stop": [P],
+    "wj_train_epoch": [P, P, P, P, I32, I64, I32, P, P, I32, P, P, I64, P, P, P, P],
 }
 
 _lib = None

@@ -23,6 +23,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <memory>
+#include <exception>
 #include <thread>
 #include <cstdlib>
 #include <cstring>
@@ -95,8 +96,10 @@ inline uint64_t mix(uint64_t z) {
 // Run fn(lo, hi) over [0, n) split across up to 16 host threads (small n:
 // the calling thread alone).
 template <typename F>
-void parallel_for(int64_t n, F fn) {
-    unsigned nt = std::max(1u, std::min(std::thread::hardware_concurrency(), 16u));
+void parallel_for(int64_t n, F fn, unsigned reserve = 0) {
+    // ``reserve``: host threads left to concurrent work of the caller
+    const unsigned hc = std::max(1u, std::thread::hardware_concurrency());
+    unsigned nt = std::max(1u, std::min(hc > reserve ? hc - reserve : 1u, 16u));
     if (n < (1 << 20)) nt = 1;
     std::vector<std::thread> th;
     for (unsigned t = 1; t < nt; ++t) th.emplace_back(fn, n * t / nt, n * (t + 1) / nt);
@@ -321,19 +324,32 @@ extern "C" int wj_planner_create(const int64_t *positives, int64_t n_pos, int32_
         std::memcpy(p->pos.data(), positives, sizeof(int64_t) * n_pos * arity);
         if (n_pool > 0) p->pool.assign(neg_pool, neg_pool + n_pool * arity);
         // node -> qids (QueryOverlapIndex, pipeline.py:54-69): counting sort in
-        // qid order keeps each node's list ascending, repeats included
-        p->node_off.allocate(num_nodes + 1);
-        p->node_off.fill(0);
-        for (int64_t i = 0; i < n_pos * arity; ++i) p->node_off[positives[i] + 1]++;
-        for (int64_t u = 0; u < num_nodes; ++u) {
-            if (p->node_off[u + 1] > 0) p->nodes.push_back(u);
-            p->node_off[u + 1] += p->node_off[u];
-        }
-        p->node_qids.allocate(n_pos * arity);
-        std::vector<int64_t> fillp(p->node_off.data(), p->node_off.data() + num_nodes);
-        for (int64_t q = 0; q < n_pos; ++q)
-            for (int a = 0; a < arity; ++a) p->node_qids[fillp[positives[q * arity + a]]++] = q;
-        lap("validate + query index");
+        // qid order keeps each node's list ascending, repeats included.  It
+        // runs on its own thread while the filter set is built in parallel.
+        std::exception_ptr index_err;
+        std::thread index_thread([&]() {
+            try {
+                p->node_off.allocate(num_nodes + 1);
+                p->node_off.fill(0);
+                for (int64_t i = 0; i < n_pos * arity; ++i) p->node_off[positives[i] + 1]++;
+                for (int64_t u = 0; u < num_nodes; ++u) {
+                    if (p->node_off[u + 1] > 0) p->nodes.push_back(u);
+                    p->node_off[u + 1] += p->node_off[u];
+                }
+                p->node_qids.allocate(n_pos * arity);
+                std::vector<int64_t> fillp(p->node_off.data(), p->node_off.data() + num_nodes);
+                for (int64_t q = 0; q < n_pos; ++q)
+                    for (int a = 0; a < arity; ++a) p->node_qids[fillp[positives[q * arity + a]]++] = q;
+            } catch (...) {
+                index_err = std::current_exception();
+            }
+        });
+        struct Joiner {
+            std::thread &t;
+            ~Joiner() {
+                if (t.joinable()) t.join();
+            }
+        } joiner{index_thread};
         if (arity <= 2) {
             p->filter1.reserve(n_filter);
             lap("filter table allocate + clear");
@@ -350,12 +366,14 @@ extern "C" int wj_planner_create(const int64_t *positives, int64_t n_pos, int32_
                     if (i + D < hi) __builtin_prefetch(&p->filter1.slots[p->filter1.slot_of(key(i + D))], 1);
                     p->filter1.insert_atomic(key(i));
                 }
-            });
+            }, 1);
         } else {
             p->filter2.reserve(n_filter);
             for (int64_t i = 0; i < n_filter; ++i) p->filter2.insert(pack2(filter_tuples + i * arity, arity));
         }
-        lap("filter insert");
+        index_thread.join();
+        if (index_err) std::rethrow_exception(index_err);
+        lap("filter insert + query index");
         p->seed_stamp.allocate(num_nodes);
         p->seed_stamp.fill(0);
         p->batch_stamp.allocate(n_pos);

@@ -253,6 +253,7 @@ class BatchPlanner:
         pl = None if pool is None or len(pool) == 0 else np.ascontiguousarray(pool, dtype=np.int64)
         self._lib = _lib.load()
         self.rng, self.arity = rng, int(pos.shape[1])
+        self.n_pos = int(pos.shape[0])
         self.cap = int(cfg.batch_size) * (1 + int(cfg.k_neg))
         self._h = ctypes.c_void_p()
         cargs = (pos.ctypes.data, pos.shape[0], self.arity, filt.ctypes.data, filt.shape[0], int(num_nodes),
@@ -369,6 +370,23 @@ class BatchPlanner:
             if self._running:
                 self._lib.wj_planner_stop(self._h)
                 self._running = False
+
+    def start_native(self) -> None:
+        """Start an epoch's producer thread for a native consumer
+        (``TrainStep.run_epoch`` / wj_train_epoch) instead of ``epoch()``."""
+        from . import _lib
+
+        self.wait()
+        _lib.call("wj_planner_start_epoch", self._h, self._q.data_ptr(), self._y.data_ptr(), self._g.data_ptr(),
+                  self.depth, self.cap)
+        self._running = True
+
+    def end_native(self, stopped: bool) -> None:
+        """After a native epoch: the producer returned (epoch complete) or is
+        stopped here (the consumer ended early)."""
+        if stopped:
+            self._lib.wj_planner_stop(self._h)
+        self._running = False
 
     def sync(self) -> None:
         """Write the planner's PCG64 state back into the numpy generator."""
@@ -712,6 +730,54 @@ class TrainStep:
         self.params.version += 1
         return out
 
+    def run_epoch(self, planner: "BatchPlanner", loss_out: Optional[torch.Tensor] = None,
+                  max_steps: int = -1, device_depth: int = 4) -> int:
+        """One epoch (or ``max_steps`` batches) of the native planner through
+        the step executor with no Python between steps (wj_train_epoch):
+        pinned planner slot -> H2D one batch ahead on a copy stream -> step ->
+        loss into ``loss_out[k]`` (device or pinned host, float32; default: a
+        device buffer, see ``epoch_losses``).  Same batches, kernels and
+        results as iterating ``DeviceFeeder.epoch()`` with ``__call__``.
+        Single process, chain launch only.  Returns the number of steps."""
+        from . import _lib
+
+        if self.launch != "chain" or self.group is not None:
+            raise ValueError("run_epoch needs launch='chain' and no process group")
+        cap, A = planner.cap, planner.arity
+        if self._stepper is None or cap > self._stepper_cap:
+            self._make_stepper(cap)
+        ring = getattr(self, "_ering", None)
+        if ring is None or ring[0].shape[1] != cap or ring[0].shape[2] != A or ring[0].shape[0] != device_depth:
+            lab = torch.zeros(2 * cap, dtype=torch.float32, device=self.dev)
+            lab[:cap] = 1.0
+            ring = (torch.empty((device_depth, cap, A), dtype=torch.int64, device=self.dev),
+                    torch.empty((device_depth, (2 + A) * cap + 2), dtype=torch.int32, device=self.dev), lab,
+                    torch.cuda.Stream(self.dev))
+            self._ering = ring
+        dq, dg, lab, cstream = ring
+        if loss_out is None:
+            n = max_steps if max_steps >= 0 else planner.n_pos + 1
+            if getattr(self, "epoch_losses", None) is None or self.epoch_losses.numel() < n:
+                self.epoch_losses = torch.empty(n, dtype=torch.float32, device=self.dev)
+            loss_out = self.epoch_losses
+        done, nbytes = ctypes.c_int64(0), ctypes.c_int64(0)
+        planner.start_native()
+        try:
+            _lib.call("wj_train_epoch", self._stepper, planner._h, planner._q.data_ptr(), planner._g.data_ptr(),
+                      planner.depth, cap, A, dq.data_ptr(), dg.data_ptr(), device_depth, lab.data_ptr(),
+                      loss_out.data_ptr(), int(max_steps), _lib.stream_handle(self.dev), cstream.cuda_stream,
+                      ctypes.byref(done), ctypes.byref(nbytes))
+        except BaseException:
+            planner.end_native(stopped=True)
+            raise
+        k = int(done.value)
+        self.last_epoch_h2d_bytes = int(nbytes.value)  # batches issued (incl. one look-ahead copy)
+        planner.end_native(stopped=max_steps >= 0 and k >= max_steps)
+        self.state.step += k
+        self._n_calls += k
+        self.params.version += k
+        return k
+
     def encode_only(self, q: torch.Tensor, groups=None) -> None:
         """Chain mode: launch just this step's join+encode kernel (same
         plan, scheduling and buffers; the step counter is not advanced)."""
@@ -954,7 +1020,12 @@ def train(store: SubgraphStore, split, cfg: TrainConfig, features=None, train_ne
         t0 = time.perf_counter()
         consumed, n_steps = 0, 0
         loss_sum = torch.zeros((), dtype=torch.float64, device=dev)
-        if planner is not None and step.launch == "chain":
+        if planner is not None and step.launch == "chain" and step.group is None:
+            # the native epoch loop: planner -> H2D -> chain executor with no
+            # Python between steps; per-step losses in a device buffer
+            n_steps = step.run_epoch(planner)
+            loss_sum += step.epoch_losses[:n_steps].double().sum()
+        elif planner is not None and step.launch == "chain":
             # native planner -> device ring -> chain executor; per-step losses
             # stay in the executor's ring and are summed in blocks
             pending = []

@@ -192,3 +192,48 @@ def test_chain_equals_graph_hyperedges():
     assert outs[0][0] == outs[1][0]
     for k in outs[0][1]:
         assert torch.equal(outs[0][1][k], outs[1][1][k]), k
+
+
+@pytest.mark.parametrize("max_steps", [-1, 5])
+def test_native_epoch_equals_python_loop(max_steps):
+    """TrainStep.run_epoch (wj_train_epoch: planner -> H2D -> step executor,
+    no Python between steps) == the DeviceFeeder + per-step chain loop: same
+    batches, losses and parameters bit for bit, and the planner's generator
+    ends in the same state."""
+    import paper_2202_13538_b200 as wj
+    from paper_2202_13538_b200.pipeline import BatchPlanner, DeviceFeeder, TrainConfig
+
+    rng = np.random.default_rng(11)
+    n = 2000
+    g = wj.Graph.from_edges(rng.integers(0, n, size=(16000, 2)), n)
+    s = wj.preprocess(g, 40, 4, 5)
+    pos = np.stack([rng.choice(n, 2, replace=False) for _ in range(700)]).astype(np.int64)
+    cfg = TrainConfig(batch_size=16, k_neg=7)
+    outs = []
+    for native in (False, True):
+        planner = BatchPlanner(pos, pos, n, cfg, np.random.default_rng(3), depth=4)
+        p = wj.init_params(2, 4, dropout=0.1, seed=9)
+        st = wj.AdamState.for_params(p)
+        step = wj.TrainStep(s, p, st, seed=21, launch="chain")
+        if native:
+            k = step.run_epoch(planner, max_steps=max_steps)
+            losses = step.epoch_losses[:k].cpu().tolist()
+        else:
+            feeder = DeviceFeeder(planner, torch.device("cuda", 0))
+            losses = []
+            it = feeder.epoch()
+            for q, y, _ in it:
+                losses.append(float(step(q, y, groups=(feeder.groups, feeder.n_groups))))
+                feeder.consumed()
+                if max_steps >= 0 and len(losses) == max_steps:
+                    break
+            it.close()
+        torch.cuda.synchronize()
+        planner.close()
+        outs.append((losses, {k_: v.clone() for k_, v in p.tensors.items()}, int(step.step_t.item()),
+                     planner.rng.bit_generator.state["state"]["state"] if max_steps < 0 else None))
+    (l0, p0, t0, r0), (l1, p1, t1, r1) = outs
+    assert len(l0) == len(l1) > 3 and l0 == l1
+    assert t0 == t1 == len(l0)
+    assert all(torch.equal(p0[k], p1[k]) for k in p0)
+    assert r0 == r1
