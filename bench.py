@@ -90,6 +90,10 @@ def parse():
     ap.add_argument("--pre", default="sharded", choices=["sharded", "redundant"],
                     help="N>1 preprocess: node-range shards + NCCL all-gathers, or the full store on every rank "
                          "(no communication; SURVEY 8(e) asks for both)")
+    ap.add_argument("--dp", default="replicate", choices=["replicate", "shard"],
+                    help="N>1 training: replicate = each rank steps its own reference batches and the gradients "
+                         "are averaged (weak scaling, effective batch x N); shard = every reference batch is split "
+                         "over the ranks (the single-GPU step's semantics, bit-identical; strong scaling)")
     ap.add_argument("--launch", default="chain", choices=["chain", "graph"],
                     help="chain: native step executor, PDL-chained across steps; graph: one CUDA graph per step")
     ap.add_argument("--mode", default="fused", choices=["fused", "pooled", "reference"],
@@ -357,10 +361,17 @@ def run_ours(args, cfg):
     from paper_2202_13538_b200 import _lib
 
     world, rank, local = dist_env()
+    # WJ_DIST_BACKEND=gloo runs the N>1 code path with several ranks on one
+    # GPU (functional check on a one-GPU box; NCCL needs one GPU per rank)
+    backend = os.environ.get("WJ_DIST_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1) if backend == "gloo" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     _lib.load()
     torch.manual_seed(1234 + rank)
 
@@ -433,7 +444,10 @@ def run_ours_train(args, cfg, store, ctx):
 
     # ---- batch plan (host), uploaded before the timed region
     W, K = args.warmup, args.steps
-    plan = make_plan(wl, W + K, BATCH_SEED + rank)
+    shard = world > 1 and args.dp == "shard"  # one batch stream split over the ranks
+    bseed = BATCH_SEED if shard else BATCH_SEED + rank
+    per_rank_batches = nb_epoch if shard else nb_epoch / world
+    plan = make_plan(wl, W + K, bseed)
     qd = [torch.from_numpy(q).to(dev) for q, _ in plan]
     yd = [torch.from_numpy(y).to(dev) for _, y in plan]
     gd = []  # the planner's per-batch groups of identical queries (wj_group_queries)
@@ -446,8 +460,9 @@ def run_ours_train(args, cfg, store, ctx):
     pg = dist.group.WORLD if world > 1 else None
     params = wj.init_params(A, L, hidden=64, dropout=0.1, seed=11, device=dev)
     state = wj.AdamState.for_params(params, lr=1e-3)
+    sseed = 1000 if shard else 1000 + rank
     step = wj.TrainStep(store, params, state, dense_dtype=torch.float32, mode=args.mode, use_graph=True,
-                        process_group=pg, seed=1000 + rank, overlap_inputs=True, launch=args.launch)
+                        process_group=pg, seed=sseed, overlap_inputs=True, launch=args.launch, dp_mode=args.dp)
     for k in range(W):                       # warm-up: captures every batch shape of the plan
         step(qd[k], yd[k], groups=gd[k])
     for k in range(W, W + K):
@@ -518,7 +533,7 @@ def run_ours_train(args, cfg, store, ctx):
     e0.record()
     planner = BatchPlanner(wl.train_pos, wl.filter_rows, wl.n,
                            TrainConfig(batch_size=POS_PER_BATCH, k_neg=cfg["k_neg"]),
-                           np.random.default_rng(BATCH_SEED + rank), depth=8, background=True)
+                           np.random.default_rng(bseed), depth=8, background=True)
     store = wl.prep(host_g, sharded=world > 1 and args.pre == "sharded" and wl.edge_types is None)
     e1.record()
     torch.cuda.synchronize()
@@ -531,8 +546,8 @@ def run_ours_train(args, cfg, store, ctx):
     params = wj.init_params(A, L, hidden=64, dropout=0.1, seed=11, device=dev)
     state = wj.AdamState.for_params(params, lr=1e-3)
     step = wj.TrainStep(store, params, state, dense_dtype=torch.float32, mode=args.mode, use_graph=True,
-                        process_group=pg, seed=1000 + rank, overlap_inputs=True, launch=args.launch)
-    n_e2e = K if args.no_epoch else nb_epoch // world
+                        process_group=pg, seed=sseed, overlap_inputs=True, launch=args.launch, dp_mode=args.dp)
+    n_e2e = K if args.no_epoch else int(per_rank_batches)
     loss_h = torch.empty(W + max(n_e2e, 1), dtype=torch.float32).pin_memory()
     chain = step.launch == "chain"
     # chain: pinned batch -> side-stream H2D into a device ring (one batch
@@ -590,7 +605,7 @@ def run_ours_train(args, cfg, store, ctx):
     t_run_e2e = max_over_ranks(max(t_dev_e2e, wall))
     h2d = int(h2d_total / max(steps_done, 1))
     if args.no_epoch:
-        e2e = q_epoch / (t_pre_e2e + (nb_epoch / world) * t_run_e2e / max(steps_done, 1))
+        e2e = q_epoch / (t_pre_e2e + per_rank_batches * t_run_e2e / max(steps_done, 1))
     else:
         e2e = q_epoch / (t_pre_e2e + t_run_e2e)
 
@@ -603,7 +618,7 @@ def run_ours_train(args, cfg, store, ctx):
     else:
         launches_per_step = 1
         launches_note = "per timed step: wj_join (the encoder runs as PyTorch/cuBLAS kernels)"
-    value = q_epoch / (t_pre + (nb_epoch / world) * t_step)
+    value = q_epoch / (t_pre + per_rank_batches * t_step)
 
     # ---- roofline of the dominant kernel
     hbm, peak_kind = peaks()
@@ -618,15 +633,17 @@ def run_ours_train(args, cfg, store, ctx):
         "warmup": W,
         "ms_per_step": round(t_step * 1e3, 4),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if shard else "weak",
         "vs_baseline": None,
         "dtype": "int32 walk/RPE/join, fp32 encoder",
         "data": "synthetic (graph of the named shape, random-init encoder)",
         "config": _common_config(cfg, wl, store, ctx, {
             "queries_per_step": B_mean, "train_pos": int(wl.train_pos.shape[0]), "k_neg": cfg["k_neg"],
             "Q_epoch": q_epoch, "batches_per_epoch": nb_epoch,
-            "value_formula": "Q_epoch / (t_pre + batches_per_epoch / n_gpus * t_step)",
-            "final_loss": final_loss, "parallelism": f"dp{world}", "launch": args.launch,
+            "value_formula": ("Q_epoch / (t_pre + batches_per_epoch * t_step)" if shard else
+                              "Q_epoch / (t_pre + batches_per_epoch / n_gpus * t_step)"),
+            "final_loss": final_loss, "parallelism": f"dp{world}" + (f" ({args.dp})" if world > 1 else ""),
+            "launch": args.launch,
             "preprocess": args.pre if world > 1 else "single"}),
         "e2e": {"value": round(e2e, 1), "unit": "queries/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": 4, "t_pre_ms": round(t_pre_e2e * 1e3, 3),

@@ -278,6 +278,18 @@ int wj_stepper_encode(wj_stepper *stepper, const int64_t *queries, int64_t n_bat
 int wj_stepper_grads(wj_stepper *stepper, const int64_t *queries, const float *labels, int64_t n_batch,
                      const int32_t *groups, int64_t n_groups, float *grad_out, wj_stream_t stream);
 int wj_stepper_apply(wj_stepper *stepper, const float *grad, float *loss_out, wj_stream_t stream);
+/* Batch-sharded data parallel (one reference mini-batch over P
+ * ranks): rank r runs queries [b_offset, b_offset + n_batch) of a global batch
+ * of b_global queries whose single-GPU tail rows of per_cta queries are rows
+ * [b_offset / per_cta, + rows): join+encode with the global dropout keys, the
+ * tail with the global 1/B into partial_out [rows, n_params + 1].  Gathering
+ * every rank's rows in order and applying them (wj_stepper_apply_rows) is
+ * bit-identical to wj_stepper_run on the whole batch. */
+int wj_stepper_grads_shard(wj_stepper *stepper, const int64_t *queries, const float *labels, int64_t n_batch,
+                           const int32_t *groups, int64_t n_groups, int64_t b_offset, int64_t b_global,
+                           int32_t per_cta, int32_t rows, float *partial_out, wj_stream_t stream);
+int wj_stepper_apply_rows(wj_stepper *stepper, const float *partial, int32_t rows, float *loss_out,
+                          wj_stream_t stream);
 int wj_stepper_destroy(wj_stepper *stepper);
 
 /* Fixed-order column sums out[c] = sum_r partial[r, c] of a [rows, n_cols]

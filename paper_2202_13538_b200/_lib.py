@@ -53,6 +53,8 @@ SIGNATURES = {
     "wj_stepper_encode": [P, P, I64, P, I64, P],
     "wj_stepper_grads": [P, P, P, I64, P, I64, P, P],
     "wj_stepper_apply": [P, P, P, P],
+    "wj_stepper_grads_shard": [P, P, P, I64, P, I64, I64, I64, I32, I32, P, P],
+    "wj_stepper_apply_rows": [P, P, I32, P, P],
     "wj_gather_rpe": [P, I64, P, I64, I32, P, I32, P, P],
     "wj_export_dicts": [P, P, P, P, P, I64, I32, I32, P, P, P, P],
     "wj_lookup": [P, P, I64, P, P, P, P, P],

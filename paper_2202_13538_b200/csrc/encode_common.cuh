@@ -48,6 +48,7 @@ struct EncMmaArgs {
     // reduction per member (each with its own dropout stream and outputs)
     const int32_t *groups;
     int64_t n_units;  // G with groups, else n_batch
+    int64_t b_offset;  // index of query 0 in the global batch (dropout key; batch-sharded data parallel)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {

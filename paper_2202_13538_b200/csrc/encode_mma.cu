@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
             __syncthreads();
         }
         // ---- per-warp tiles of 16 virtual landings
-        uint32_t qq = (uint32_t)mix64(skey ^ mix64((uint64_t)b));
+        uint32_t qq = (uint32_t)mix64(skey ^ mix64((uint64_t)(b + g.b_offset)));
         qq ^= qq >> 16;
         float sacc[4][2][4];
 #pragma unroll
@@ -865,6 +865,53 @@ extern "C" int wj_stepper_grads(wj_stepper *st, const int64_t *queries, const fl
                              st->scale, nullptr, st->partial, (int32_t)rows, nullptr, st->step, stream);
     if (rc != WJ_OK) return rc;
     return wj_sum_partials(st->partial, (int32_t)rows, st->n_params + 1, grad_out, stream);
+}
+
+namespace wj {
+int encoder_tail(const float *, const float *, const float *, const float *, int64_t, int32_t, int32_t, const float *,
+                 const int32_t *, float, float *, float *, int32_t, int32_t, float, int64_t *, cudaStream_t);
+}
+
+// Batch-sharded data parallel: this rank's slice of one global
+// batch -- queries [b_offset, b_offset + n_batch) of b_global, whose tail rows
+// are rows [b_offset / per_cta, + rows) of the single-GPU step's partial rows
+// -- with the global dropout keys and the global 1/B; the caller gathers every
+// rank's rows in order and applies them with wj_stepper_apply_rows, which is
+// then bit-identical to wj_stepper_run on the whole batch.
+extern "C" int wj_stepper_grads_shard(wj_stepper *st, const int64_t *queries, const float *labels, int64_t n_batch,
+                                      const int32_t *groups, int64_t n_groups, int64_t b_offset, int64_t b_global,
+                                      int32_t per_cta, int32_t rows, float *partial_out, wj_stream_t stream) {
+    using namespace wj;
+    if (!st || n_batch < 0 || b_offset < 0 || b_global < 1 || per_cta < 1 || rows < 0 || !partial_out ||
+        (n_batch > 0 && (!queries || !labels || rows < 1))) {
+        set_error("wj_stepper_grads_shard: bad arguments");
+        return WJ_ERR_ARG;
+    }
+    if (n_batch == 0) return WJ_OK;
+    if (rows > st->tail_rows_max) {
+        set_error("wj_stepper_grads_shard: %d rows exceed the stepper's %d", rows, st->tail_rows_max);
+        return WJ_ERR_ARG;
+    }
+    st->args.b_offset = b_offset;
+    const int rc0 = wj_stepper_encode(st, queries, n_batch, groups, n_groups, stream);
+    st->args.b_offset = 0;
+    if (rc0 != WJ_OK) return rc0;
+    EncMmaArgs g = st->args;
+    return encoder_tail(g.pooled, g.s_out, g.msum, labels, n_batch, st->aw, 64, st->params, st->offsets9, st->scale,
+                        nullptr, partial_out, rows, per_cta, 1.f / (float)b_global, st->step,
+                        (cudaStream_t)stream);
+}
+
+// Adam on the gathered partial rows of a batch-sharded step (fixed order)
+extern "C" int wj_stepper_apply_rows(wj_stepper *st, const float *partial, int32_t rows, float *loss_out,
+                                     wj_stream_t stream) {
+    using namespace wj;
+    if (!st || !partial || rows < 1) {
+        set_error("wj_stepper_apply_rows: bad arguments");
+        return WJ_ERR_ARG;
+    }
+    return wj_adam(st->params, st->m, st->v, partial, rows, st->n_params, st->lr, st->beta1, st->beta2, st->eps,
+                   st->step, nullptr, loss_out, stream);
 }
 
 extern "C" int wj_stepper_apply(wj_stepper *st, const float *grad, float *loss_out, wj_stream_t stream) {

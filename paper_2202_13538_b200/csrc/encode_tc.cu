@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, MINB) join_encode_tc_kernel(EncM
 
         for (int mem = 0; mem < mcount; ++mem) {
             if (mem > 0) b = gorder[mstart + mem];
-            uint32_t qq = (uint32_t)mix64(skey ^ mix64((uint64_t)b));
+            uint32_t qq = (uint32_t)mix64(skey ^ mix64((uint64_t)(b + g.b_offset)));
             qq ^= qq >> 16;
             // pipeline: tile i's z was issued two tiles earlier (two TMEM
             // buffers), its G goes to G buffer i & 1 once S(i - 2) has read it,

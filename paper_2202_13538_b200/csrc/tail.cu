@@ -474,12 +474,15 @@ static TailKernel pick_tail(int aw, size_t &smem) {
 
 }  // namespace wj
 
-extern "C" int wj_encoder_tail(const float *pooled, const float *s, const float *msum,
-                               const float *labels, int64_t n_batch, int32_t aw, int32_t hidden,
-                               const float *params, const int32_t *offsets9, float scale,
-                               float *logits_out, float *partial, int32_t partial_rows, float *work,
-                               int64_t *step_inc, wj_stream_t stream) {
-    using namespace wj;
+namespace wj {
+
+// training: exactly partial_rows CTAs, CTA i owns queries [i*q, (i+1)*q) with
+// q = per_cta (0: ceil(B / partial_rows)), rows past the last query are zeros;
+// inference: one CTA per 16 queries.  inv_b: the mean's 1 / B (0: 1 / n_batch).
+int encoder_tail(const float *pooled, const float *s, const float *msum, const float *labels, int64_t n_batch,
+                 int32_t aw, int32_t hidden, const float *params, const int32_t *offsets9, float scale,
+                 float *logits_out, float *partial, int32_t partial_rows, int32_t per_cta, float inv_b,
+                 int64_t *step_inc, cudaStream_t stream) {
     if (hidden != kH) {
         set_error("encoder tail kernel supports hidden=64 (got %d)", hidden);
         return WJ_ERR_UNSUPPORTED;
@@ -494,7 +497,6 @@ extern "C" int wj_encoder_tail(const float *pooled, const float *s, const float 
         set_error("training tail needs S, msum and a partial buffer");
         return WJ_ERR_ARG;
     }
-    (void)work;  // not needed by the tensor-core tail (kept for ABI stability)
     if (n_batch == 0 && !labels) return WJ_OK;
     TailArgs g;
     g.pooled = pooled;
@@ -506,16 +508,13 @@ extern "C" int wj_encoder_tail(const float *pooled, const float *s, const float 
     g.off = {offsets9[0], offsets9[1], offsets9[2], offsets9[3], offsets9[4],
              offsets9[5], offsets9[6], offsets9[7], offsets9[8]};
     g.scale = scale;
-    g.inv_b = n_batch > 0 ? 1.f / (float)n_batch : 0.f;
+    g.inv_b = inv_b > 0.f ? inv_b : (n_batch > 0 ? 1.f / (float)n_batch : 0.f);
     g.logits = logits_out;
     g.partial = partial;
     g.work = nullptr;
     g.step_inc = step_inc;
-    // training: exactly partial_rows CTAs, CTA i owns queries [i*q, (i+1)*q),
-    // q = ceil(B / partial_rows) (rows past the last query are zeros);
-    // inference: one CTA per 16 queries
     const int64_t rows = labels ? partial_rows : (n_batch + kTQ - 1) / kTQ;
-    g.per_cta = (int)((n_batch + rows - 1) / rows);
+    g.per_cta = per_cta > 0 ? per_cta : (int)((n_batch + rows - 1) / rows);
     // the smem attribute is per (device, kernel): set once (a repeat is harmless)
     static bool attr_done[64][17] = {};
     int dev = 0;
@@ -529,12 +528,24 @@ extern "C" int wj_encoder_tail(const float *pooled, const float *s, const float 
         }
         if (dev >= 0 && dev < 64) attr_done[dev][aw] = true;
     }
-    e = launch_pdl(k, dim3((unsigned)rows), dim3(kTW * 32), smem, (cudaStream_t)stream, g);
+    e = launch_pdl(k, dim3((unsigned)rows), dim3(kTW * 32), smem, stream, g);
     if (e != cudaSuccess) {
         set_error("wj_encoder_tail launch: %s", cudaGetErrorString(e));
         return WJ_ERR_CUDA;
     }
     return check_launch("wj_encoder_tail");
+}
+
+}  // namespace wj
+
+extern "C" int wj_encoder_tail(const float *pooled, const float *s, const float *msum,
+                               const float *labels, int64_t n_batch, int32_t aw, int32_t hidden,
+                               const float *params, const int32_t *offsets9, float scale,
+                               float *logits_out, float *partial, int32_t partial_rows, float *work,
+                               int64_t *step_inc, wj_stream_t stream) {
+    (void)work;  // not needed by the tensor-core tail (kept for ABI stability)
+    return wj::encoder_tail(pooled, s, msum, labels, n_batch, aw, hidden, params, offsets9, scale, logits_out,
+                            partial, partial_rows, 0, 0.f, step_inc, (cudaStream_t)stream);
 }
 
 extern "C" int wj_adam(float *params, float *m, float *v, const float *partial,

@@ -61,6 +61,37 @@ def all_gather_variable(t: torch.Tensor, group=None) -> list:
     return [b[:s] for b, s in zip(bufs, sizes)]
 
 
+def _bytes_view(t: torch.Tensor) -> torch.Tensor:
+    return t if t.dtype in _NCCL_DTYPES else t.view(torch.uint8)
+
+
+def gather_into(out: torch.Tensor, local: torch.Tensor, rows: list, group=None) -> torch.Tensor:
+    """Concatenate every rank's ``local`` (rows[j] rows on rank j) into the
+    preallocated ``out`` in rank order: one broadcast per rank straight into
+    its slice of ``out`` -- no padding, no per-rank temporaries, no second copy
+    of the store (the padded all_gather + cat this replaces held ~2x the
+    store at the citation2 shape)."""
+    rank = dist.get_rank(group)
+    off = 0
+    for j, n in enumerate(rows):
+        dst = out[off: off + n]
+        if j == rank:
+            dst.copy_(local[:n])
+        if n:
+            dist.broadcast(_bytes_view(dst), src=dist.get_global_rank(group, j) if group is not None else j,
+                           group=group)
+        off += n
+    return out
+
+
+def all_gather_sizes(n: int, device, group=None) -> list:
+    world = dist.get_world_size(group)
+    t = torch.tensor([int(n)], dtype=torch.int64, device=device)
+    sizes = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(sizes, t, group=group)
+    return [int(x.item()) for x in sizes]
+
+
 def merge_distinct(keys: torch.Tensor, orders: torch.Tensor):
     """Merge per-rank (packed vector, first scan order) pairs: min order per
     distinct vector, then ids = 1 + rank by that order.  Returns
@@ -122,15 +153,22 @@ def preprocess_sharded(g, num_walks: int, num_steps: int, seed: int, threads: in
     uk, ids, table_keys = merge_distinct(gk, go)
     uid_l = ids[torch.searchsorted(uk, ukey_l)]
     ph.mark("gather")
-    # exchange the store
-    counts = torch.cat(all_gather_variable(counts_l, group))
+    # exchange the store: every array gathered straight into its full-size
+    # buffer (fixed-size per anchor: walks / slot_idx; variable: the lists)
+    world_rows = [shard_range(n, world, j)[1] - shard_range(n, world, j)[0] for j in range(world)]
+    counts = gather_into(torch.empty(n, dtype=torch.int32, device=dev), counts_l, world_rows, group)
     offsets = torch.zeros(n + 1, dtype=torch.int64, device=dev)
     torch.cumsum(counts, 0, out=offsets[1:])
-    walks = torch.cat(all_gather_variable(walks_l, group))
-    slot = torch.cat(all_gather_variable(slot_l, group))
-    ux = torch.cat(all_gather_variable(ux_l, group))
-    uid = torch.cat(all_gather_variable(uid_l, group))
-    uf = torch.cat(all_gather_variable(uf_l, group))
+    walks = gather_into(torch.empty((n, M, W), dtype=torch.int32, device=dev), walks_l, world_rows, group)
+    del walks_l
+    slot = gather_into(torch.empty((n, P), dtype=torch.int16, device=dev), slot_l, world_rows, group)
+    del slot_l
+    ent_rows = all_gather_sizes(total_l, dev, group)
+    total = sum(ent_rows)
+    ux = gather_into(torch.empty(total, dtype=torch.int32, device=dev), ux_l, ent_rows, group)
+    uid = gather_into(torch.empty(total, dtype=torch.int32, device=dev), uid_l, ent_rows, group)
+    uf = gather_into(torch.empty(total, dtype=torch.int16, device=dev), uf_l, ent_rows, group)
+    del ux_l, uid_l, uf_l
     store = SubgraphStore(n, M, L, _u64(seed), walks, offsets, ux, uid, uf, slot, table_keys,
                           int(counts.max().item()) if n else 0, id_map=getattr(g, "id_map", None))
     ph.mark("vindex")

@@ -517,7 +517,11 @@ class TrainStep:
     def __init__(self, store: SubgraphStore, params: E.ModelParams, state: E.AdamState,
                  dense_dtype=torch.float32, mode: str = "fused", use_graph: bool = True,
                  process_group=None, seed: int = 0, fast_tail: Optional[bool] = None,
-                 features: Optional[torch.Tensor] = None, overlap_inputs: bool = False, launch: str = "graph"):
+                 features: Optional[torch.Tensor] = None, overlap_inputs: bool = False, launch: str = "graph",
+                 dp_mode: str = "replicate"):
+        if dp_mode not in ("replicate", "shard"):
+            raise ValueError(f"dp_mode must be 'replicate' or 'shard', got {dp_mode!r}")
+        self.dp_mode = dp_mode
         if features is not None and mode == "fused":
             raise ValueError("node features need mode='pooled' or 'reference' (the fused kernel is RPE-only)")
         if mode == "fused" and not E.fused_supported(params, store):
@@ -577,6 +581,9 @@ class TrainStep:
             except (NotImplementedError, ValueError):
                 self._stepper, self._stepper_cap = None, 0
                 self.launch = "graph"
+        if process_group is not None and dp_mode == "shard" and self.launch != "chain":
+            raise NotImplementedError("dp_mode='shard' needs the chain step executor (launch='chain', fused, "
+                                      "hidden 64)")
 
     def _buffers(self, B, A):
         if self.mode == "fused":
@@ -684,6 +691,11 @@ class TrainStep:
                   _lib.ptr(b["S"]), _lib.ptr(b["msum"]), _lib.ptr(b["partial"]), rows_max,
                   _lib.ptr(self._sched) if self.dynamic_queries else None, ctypes.byref(h))
         self._stepper, self._stepper_cap = h, cap
+        self._rows_max = rows_max
+        if self.group is not None and self.dp_mode == "shard":
+            n1 = int(self.offs[-1]) + 1
+            self._shard_partial = torch.empty((rows_max, n1), device=self.dev)
+            self._full_partial = torch.empty((rows_max, n1), device=self.dev)
         if self._loss_hist is None:
             self._loss_hist = torch.zeros(self._LOSS_HIST, dtype=torch.float32, device=self.dev)
 
@@ -711,6 +723,8 @@ class TrainStep:
         if self.group is None:
             _lib.call("wj_stepper_run", self._stepper, q.data_ptr(), y.data_ptr(), B, gptr, int(ng), out.data_ptr(),
                       sh)
+        elif self.dp_mode == "shard":  # one global batch sharded over the ranks
+            self._shard_step(q, y, out, sh)
         else:  # data parallel: grads + loss -> NCCL average -> Adam
             from .distributed import all_reduce_mean
 
@@ -729,6 +743,35 @@ class TrainStep:
             self.input_event = None
         self.params.version += 1
         return out
+
+    def _shard_step(self, q: torch.Tensor, y: torch.Tensor, out: torch.Tensor, sh) -> None:
+        """Batch-sharded data parallel: every rank holds the
+        same global batch and runs the queries of its share of the
+        single-GPU step's tail rows (wj_stepper_grads_shard); the ranks'
+        partial rows are gathered in row order (one broadcast per rank) and
+        every rank applies the same fixed-order Adam reduction to them, so the
+        step is bit-identical to one GPU stepping the whole batch."""
+        import torch.distributed as dist
+
+        from . import _lib
+
+        B = q.shape[0]
+        world, rank = dist.get_world_size(self.group), dist.get_rank(self.group)
+        R = max(1, min((B + 15) // 16, self._rows_max))
+        if R < world:
+            raise ValueError(f"a batch of {B} queries has {R} tail rows, fewer than the {world} ranks")
+        pc = -(-B // R)
+        bounds = [(j * R // world, (j + 1) * R // world) for j in range(world)]
+        r0, r1 = bounds[rank]
+        b0, b1 = min(B, r0 * pc), min(B, r1 * pc)
+        _lib.call("wj_stepper_grads_shard", self._stepper, q[b0:].data_ptr(), y[b0:].data_ptr(), b1 - b0, None, 0,
+                  b0, B, pc, r1 - r0, _lib.ptr(self._shard_partial), sh)
+        full = self._full_partial
+        for j, (j0, j1) in enumerate(bounds):
+            if j == rank:
+                full[j0:j1].copy_(self._shard_partial[: j1 - j0])
+            dist.broadcast(full[j0:j1], src=j, group=self.group)
+        _lib.call("wj_stepper_apply_rows", self._stepper, _lib.ptr(full), R, out.data_ptr(), sh)
 
     def run_epoch(self, planner: "BatchPlanner", loss_out: Optional[torch.Tensor] = None,
                   max_steps: int = -1, device_depth: int = 4) -> int:

@@ -35,8 +35,21 @@ def _worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from oracle import core
-        from paper_2202_13538_b200.distributed import (all_gather_variable, all_reduce_grads,
-                                                       all_reduce_mean, merge_distinct, shard_range)
+        from paper_2202_13538_b200.distributed import (all_gather_sizes, all_gather_variable, all_reduce_grads,
+                                                       all_reduce_mean, gather_into, merge_distinct, shard_range)
+
+        # 0. gather straight into a preallocated buffer (rank order, no padding;
+        # int16 as bytes; an empty shard)
+        rows = [3 + 4 * r for r in range(world)]
+        assert all_gather_sizes(rows[rank], "cpu") == rows
+        loc = torch.arange(rows[rank] * 2, dtype=torch.int16).reshape(-1, 2) - 7 * rank
+        out = gather_into(torch.empty((sum(rows), 2), dtype=torch.int16), loc, rows)
+        want = torch.cat([torch.arange(rows[r] * 2, dtype=torch.int16).reshape(-1, 2) - 7 * r for r in range(world)])
+        assert torch.equal(out, want)
+        rows0 = [0 if r == 0 else 5 for r in range(world)]
+        loc0 = torch.full((rows0[rank],), float(rank))
+        out0 = gather_into(torch.empty(sum(rows0)), loc0, rows0)
+        assert torch.equal(out0, torch.cat([torch.full((rows0[r],), float(r)) for r in range(world)]))
 
         # 1. variable-size all-gather
         t = torch.arange(3 + 4 * rank, dtype=torch.int64).reshape(-1, 1).repeat(1, 2) + 100 * rank
