@@ -20,21 +20,28 @@ constexpr int kBins = 1 << kRadixBits;
 constexpr int kRpeWarps = 8;
 
 // Stable LSD radix sort of n keys (bits [lo_bit, lo_bit+nbits)) by one warp.
-// Returns the buffer holding the result.
-template <typename K>
+// Returns the buffer holding the result.  R: rounds of 32 keys (n <= 32 * R):
+// each round's peer mask (__match_any_sync, on the ADU pipe that bounds this
+// kernel) is computed once per pass, kept in a register, and reused by the
+// histogram and the scatter.
+template <typename K, int R>
 __device__ __forceinline__ K *warp_radix_sort(K *a, K *b, int n, int lo_bit, int nbits,
                                               uint32_t *hist, int lane) {
     const unsigned lt = lanemask_lt();
     for (int shift = lo_bit; shift < lo_bit + nbits; shift += kRadixBits) {
         for (int i = lane; i < kBins; i += 32) hist[i] = 0;
         __syncwarp();
+        unsigned peers[R];
         // histogram: one smem update per distinct digit per round
-        for (int base = 0; base < n; base += 32) {
-            const int i = base + lane;
-            const uint32_t d = i < n ? (uint32_t)((a[i] >> shift) & (kBins - 1)) : 0xFFFFu;
-            const unsigned peers = __match_any_sync(kFull, d);
-            if (i < n && (peers & lt) == 0) hist[d] += __popc(peers);
-            __syncwarp();
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            if (r * 32 < n) {
+                const int i = r * 32 + lane;
+                const uint32_t d = i < n ? (uint32_t)((a[i] >> shift) & (kBins - 1)) : 0xFFFFu;
+                peers[r] = __match_any_sync(kFull, d);
+                if (i < n && (peers[r] & lt) == 0) hist[d] += __popc(peers[r]);
+                __syncwarp();
+            }
         }
         // exclusive scan over the bins, 8 per lane
         uint32_t v[kBins / 32];
@@ -59,19 +66,21 @@ __device__ __forceinline__ K *warp_radix_sort(K *a, K *b, int n, int lo_bit, int
         }
         __syncwarp();
         // stable scatter: rank inside the round = peers before me
-        for (int base = 0; base < n; base += 32) {
-            const int i = base + lane;
-            const K key = i < n ? a[i] : (K)0;
-            const uint32_t d = i < n ? (uint32_t)((key >> shift) & (kBins - 1)) : 0xFFFFu;
-            const unsigned peers = __match_any_sync(kFull, d);
-            uint32_t pos = 0;
-            if (i < n) pos = hist[d] + __popc(peers & lt);
-            __syncwarp();
-            if (i < n) {
-                b[pos] = key;
-                if ((peers & lt) == 0) hist[d] += __popc(peers);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            if (r * 32 < n) {
+                const int i = r * 32 + lane;
+                const K key = i < n ? a[i] : (K)0;
+                const uint32_t d = (uint32_t)((key >> shift) & (kBins - 1));
+                uint32_t pos = 0;
+                if (i < n) pos = hist[d] + __popc(peers[r] & lt);
+                __syncwarp();
+                if (i < n) {
+                    b[pos] = key;
+                    if ((peers[r] & lt) == 0) hist[d] += __popc(peers[r]);
+                }
+                __syncwarp();
             }
-            __syncwarp();
         }
         K *t = a;
         a = b;
@@ -87,11 +96,12 @@ struct RpeShape {
     int xbits;      // bits for node ids in [0, n)
     int cb;         // bits per packed count (counts <= M)
     uint32_t wmag;  // magic for p / W
+    uint32_t lmag;  // magic for t / L (L = W - 1)
     int pcap;       // P rounded up to a multiple of 32
 };
 
-template <typename K, bool FILL>
-__global__ void __launch_bounds__(kRpeWarps * 32) rpe_kernel(
+template <typename K, bool FILL, int R>
+__global__ void __launch_bounds__(kRpeWarps * 32, 3) rpe_kernel(
     const int32_t *__restrict__ walks, int64_t n_anchors, RpeShape sh,
     int32_t *__restrict__ counts_out, const int64_t *__restrict__ offsets,
     int32_t *__restrict__ uniq_x, uint64_t *__restrict__ uniq_key,
@@ -104,24 +114,44 @@ __global__ void __launch_bounds__(kRpeWarps * 32) rpe_kernel(
     K *bufb = bufa + sh.pcap;
     uint32_t *hist = reinterpret_cast<uint32_t *>(bufb + sh.pcap);
     const int P = sh.P;
+    const int M = sh.P / sh.W;
     const K pmask = ((K)1 << sh.pbits) - 1;
     const unsigned le = lanemask_le();
 
     for (int64_t k = (int64_t)blockIdx.x * kRpeWarps + warp; k < n_anchors;
          k += (int64_t)gridDim.x * kRpeWarps) {
         const int32_t *src = walks + k * (int64_t)P;
-        for (int i = lane; i < P; i += 32) bufa[i] = ((K)(uint32_t)__ldg(src + i) << sh.pbits) | (K)i;
+        // Every walk starts at the anchor: its M step-0 landings become ONE
+        // key (x0, p = 0) of weight M, so the sort sees M*L + 1 keys, not
+        // M*(L+1) (checked per anchor: walks given by a caller may differ)
+        const int32_t x0 = __ldg(src);
+        bool col0 = true;
+        for (int j = lane; j < M; j += 32) col0 &= __ldg(src + (int64_t)j * sh.W) == x0;
+        col0 = __all_sync(kFull, col0);
+        const int n = col0 ? M * (sh.W - 1) + 1 : P;
+        if (col0) {
+            for (int t = lane; t < n; t += 32) {
+                uint32_t p = 0;
+                if (t > 0) {
+                    const uint32_t tt = (uint32_t)t - 1, j = sh.W == 2 ? tt : fast_div16(tt, sh.lmag);
+                    p = j * sh.W + 1 + (tt - j * (sh.W - 1));
+                }
+                bufa[t] = ((K)(uint32_t)__ldg(src + p) << sh.pbits) | (K)p;
+            }
+        } else {
+            for (int i = lane; i < P; i += 32) bufa[i] = ((K)(uint32_t)__ldg(src + i) << sh.pbits) | (K)i;
+        }
         __syncwarp();
-        K *s = warp_radix_sort<K>(bufa, bufb, P, sh.pbits, sh.xbits, hist, lane);
+        K *s = warp_radix_sort<K, R>(bufa, bufb, n, sh.pbits, sh.xbits, hist, lane);
         uint16_t *slot = reinterpret_cast<uint16_t *>(s == bufa ? bufb : bufa);
 
         int carry = 0;               // heads so far
         uint64_t scarry = 0;         // running inclusive sum of count increments
         uint64_t seg_base_carry = 0; // exclusive prefix at the open segment's head
         const int64_t off = FILL ? offsets[k] : 0;
-        for (int base = 0; base < P; base += 32) {
+        for (int base = 0; base < n; base += 32) {
             const int i = base + lane;
-            const bool valid = i < P;
+            const bool valid = i < n;
             const K key = valid ? s[i] : (K)0;
             const K x = key >> sh.pbits;
             const bool head = valid && (i == 0 || (s[i - 1] >> sh.pbits) != x);
@@ -130,9 +160,10 @@ __global__ void __launch_bounds__(kRpeWarps * 32) rpe_kernel(
             carry += __popc(hb);
             if (FILL) {
                 const uint32_t p = (uint32_t)(key & pmask);
-                const bool tail = valid && (i == P - 1 || (s[i + 1] >> sh.pbits) != x);
+                const bool tail = valid && (i == n - 1 || (s[i + 1] >> sh.pbits) != x);
                 const uint32_t step = p - fast_div16(p, sh.wmag) * sh.W;
                 uint64_t v = valid ? (1ULL << (sh.cb * step)) : 0ULL;
+                if (col0 && valid && p == 0) v = (uint64_t)M;  // the anchor's M step-0 landings
                 // inclusive warp scan of v
                 uint64_t incl = v;
 #pragma unroll
@@ -160,6 +191,11 @@ __global__ void __launch_bounds__(kRpeWarps * 32) rpe_kernel(
         }
         if (FILL) {
             __syncwarp();
+            if (col0) {  // every step-0 slot holds the anchor: its unique index
+                const uint16_t ru = slot[0];
+                for (int j = lane + 1; j < M; j += 32) slot[j * sh.W] = ru;
+                __syncwarp();
+            }
             uint16_t *dst = slot_idx + k * (int64_t)P;
             for (int i = lane; i < P; i += 32) dst[i] = slot[i];
         } else if (lane == 0) {
@@ -232,19 +268,20 @@ static int make_shape(int32_t M, int32_t L, int64_t n_nodes, RpeShape &sh, bool 
         return WJ_ERR_UNSUPPORTED;
     }
     sh.wmag = div_magic((uint32_t)sh.W);
+    sh.lmag = div_magic((uint32_t)L);
     sh.pcap = (sh.P + 31) / 32 * 32;
     wide = sh.pbits + sh.xbits > 32;
     return WJ_OK;
 }
 
-template <typename K, bool FILL>
-static int launch_rpe(const int32_t *walks, int64_t n_anchors, const RpeShape &sh,
+template <typename K, bool FILL, int R>
+static int launch_rpe_r(const int32_t *walks, int64_t n_anchors, const RpeShape &sh,
                       int32_t *counts, const int64_t *offsets, int32_t *ux, uint64_t *ukey,
                       uint16_t *ufirst, uint16_t *slot, cudaStream_t s) {
     if (n_anchors == 0) return WJ_OK;
     const size_t per_warp = 2 * (size_t)sh.pcap * sizeof(K) + kBins * sizeof(uint32_t);
     const size_t smem = per_warp * kRpeWarps;
-    auto kern = rpe_kernel<K, FILL>;
+    auto kern = rpe_kernel<K, FILL, R>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) {
         set_error("rpe smem attribute (%zu B): %s", smem, cudaGetErrorString(e));
@@ -259,6 +296,19 @@ static int launch_rpe(const int32_t *walks, int64_t n_anchors, const RpeShape &s
     kern<<<(unsigned)blocks, kRpeWarps * 32, smem, s>>>(walks, n_anchors, sh, counts, offsets, ux,
                                                          ukey, ufirst, slot);
     return check_launch(FILL ? "wj_rpe_fill" : "wj_rpe_count");
+}
+
+// rounds of 32 landings held in registers by the sort: 8, 16, 32, 64 or 128
+template <typename K, bool FILL>
+static int launch_rpe(const int32_t *walks, int64_t n_anchors, const RpeShape &sh, int32_t *counts,
+                      const int64_t *offsets, int32_t *ux, uint64_t *ukey, uint16_t *ufirst, uint16_t *slot,
+                      cudaStream_t s) {
+    const int rounds = sh.pcap / 32;
+    if (rounds <= 8) return launch_rpe_r<K, FILL, 8>(walks, n_anchors, sh, counts, offsets, ux, ukey, ufirst, slot, s);
+    if (rounds <= 16) return launch_rpe_r<K, FILL, 16>(walks, n_anchors, sh, counts, offsets, ux, ukey, ufirst, slot, s);
+    if (rounds <= 32) return launch_rpe_r<K, FILL, 32>(walks, n_anchors, sh, counts, offsets, ux, ukey, ufirst, slot, s);
+    if (rounds <= 64) return launch_rpe_r<K, FILL, 64>(walks, n_anchors, sh, counts, offsets, ux, ukey, ufirst, slot, s);
+    return launch_rpe_r<K, FILL, 128>(walks, n_anchors, sh, counts, offsets, ux, ukey, ufirst, slot, s);
 }
 
 }  // namespace wj
