@@ -20,8 +20,10 @@
 //  * z^T = W1aug^T [X | 1]^T is one m16n8k16 HMMA per 16 units x 8 landings
 //    (W1 and b1 as a power-of-two-scaled fp16 hi + lo pair: ~22 mantissa
 //    bits, fp32 accumulation); only z's SIGN is used;
-//  * dropout, branch-free in 16-bit SIMD lanes: one 32-bit hash gives two
-//    14-bit uniforms u (landing pair 2tq, 2tq+1 of one unit) as u' = 0x3FFF-u;
+//  * dropout, branch-free in 16-bit SIMD lanes: per lane and tile one hashed
+//    seed, then per (t, mt, hb) one IMAD (an LCG jumped ahead) gives 32 bits,
+//    folded to two 14-bit uniforms u (landing pair 2tq, 2tq+1 of one unit) as
+//    u' = 0x3FFF-u;
 //    T + u' has bit 14 set iff u < T, so the kept-row count of a lane as an
 //    fp16 value 2*K is (T1 + u') & 0x4000 (& ~sign(z)) [+ the same with T2
 //    for 2-row landings, one HADD2].  The sign mask comes from a PRMT
@@ -41,6 +43,22 @@
 #include "encode_common.cuh"
 
 namespace wj {
+
+// Dropout stream: per lane and tile one hashed 32-bit seed s, then the 16
+// draws x_k = A_k s + C_k (k = 0..15) = the LCG x <- a x + c (a = 747796405,
+// c = 2891336453; L'Ecuyer's multiplier, odd increment) jumped k + 1 steps
+// ahead -- one IMAD per 32 bits instead of a full hash (the integer ALU pipe
+// bounds the kernel's tiles).
+__host__ __device__ constexpr uint32_t lcg_mul(int k) {  // a^(k+1) mod 2^32
+    uint32_t A = 1u;
+    for (int i = 0; i <= k; ++i) A *= 747796405u;
+    return A;
+}
+__host__ __device__ constexpr uint32_t lcg_add(int k) {  // c (a^(k+1) - 1) / (a - 1) mod 2^32
+    uint32_t C = 0u;
+    for (int i = 0; i <= k; ++i) C = C * 747796405u + 2891336453u;
+    return C;
+}
 
 __device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
@@ -79,7 +97,11 @@ __device__ __forceinline__ void tile(const uint16_t *lst, uint32_t xr_s, uint32_
     uint32_t bx[4], bt[4];
     ldsm_x4(bx, row_addr(xr_s, ib, (lane >> 3) & 1));
     ldsm_x4_t(bt, row_addr(xr_s, it, lane >> 4));
-    const uint32_t cqk = cq * 0x7feb352dU;
+    // one full hash of the lane's tile counter per tile seeds its 16 draws
+    uint32_t seed = cq * 0x7feb352dU;
+    seed ^= seed >> 15;
+    seed *= 0x846ca68bU;
+    seed ^= seed >> 16;
     uint32_t nw[2] = {0u, 0u};
     if (KIND == 0) {  // (2 n_l, 2 n_l') of landings 8t + 2tq, 8t + 2tq + 1
         nw[0] = nl2[(lane & 3)];
@@ -106,11 +128,11 @@ __device__ __forceinline__ void tile(const uint16_t *lst, uint32_t xr_s, uint32_
                     ga[mt][2 * t + hb] = nw[t] & ~neg;
                     continue;
                 }
-                // hash of cq + counter (t, mt, hb): the first multiply and the
-                // counter fold into one IMAD with a compile-time addend
-                uint32_t x = cqk + ((uint32_t)t << 8 | (uint32_t)mt << 4 | (uint32_t)hb << 3) * 0x7feb352dU;
-                x ^= x >> 15;
-                x *= 0x846ca68bU;
+                // 32 random bits for (t, mt, hb): step k = 8t + 2mt + hb of an
+                // LCG seeded by the lane's hashed tile counter, as one IMAD by
+                // jump-ahead constants (x_k = A_k s + C_k), folded like the seed
+                const int k = 8 * t + 2 * mt + hb;
+                uint32_t x = seed * lcg_mul(k) + lcg_add(k);
                 const uint32_t up = ~(x ^ (x >> 16)) & 0x3FFF3FFFu;  // 0x3FFF - u, two lanes
                 // 0xFFFF in a lane whose z is negative (sign byte replicated)
                 const uint32_t neg = prmt(__float_as_uint(z[2 * hb]), __float_as_uint(z[2 * hb + 1]), 0xFFBBu);

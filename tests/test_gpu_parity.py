@@ -347,6 +347,19 @@ def _hash32(x):
     return x
 
 
+def _lcg_jump_tables():
+    a, c, A, C = 747796405, 2891336453, 1, 0
+    ta, tc = [], []
+    for _ in range(16):
+        A, C = (A * a) & _M32, (C * a + c) & _M32
+        ta.append(A)
+        tc.append(C)
+    return np.array(ta, dtype=np.uint64), np.array(tc, dtype=np.uint64)
+
+
+_LCG_A, _LCG_C = _lcg_jump_tables()
+
+
 def _thresholds14(keep):
     """14-bit inverse-CDF thresholds of the tensor-core kernel:
     (1-row P(K>=1), 2-row P(K>=1), 2-row P(K>=2))."""
@@ -416,10 +429,14 @@ def _fused_model_mma(store, q, w1, b1, keep, seed, step):
         v0 = v & ~np.uint64(15)
         tt = (v >> np.uint64(3)) & np.uint64(1)
         cq = (np.uint64(qq) ^ (v0 << np.uint64(5)) ^ (tq << np.uint64(6)) ^ gq) & np.uint64(_M32)
-        k = (tt << np.uint64(8)) | (mt << np.uint64(4)) | (hb << np.uint64(3))
-        x = ((cq + k) * np.uint64(0x7FEB352D)) & np.uint64(_M32)
-        x ^= x >> np.uint64(15)
-        x = (x * np.uint64(0x846CA68B)) & np.uint64(_M32)
+        # per (lane, tile) seed = one full hash of cq; draw k = 8t + 2mt + hb is
+        # the LCG (a = 747796405, c = 2891336453) jumped k + 1 steps ahead
+        sd = (cq * np.uint64(0x7FEB352D)) & np.uint64(_M32)
+        sd ^= sd >> np.uint64(15)
+        sd = (sd * np.uint64(0x846CA68B)) & np.uint64(_M32)
+        sd ^= sd >> np.uint64(16)
+        k = (np.uint64(8) * tt + np.uint64(2) * mt + hb).astype(np.int64)
+        x = (sd * _LCG_A[k] + _LCG_C[k]) & np.uint64(_M32)
         y = ~(x ^ (x >> np.uint64(16))) & np.uint64(0x3FFF3FFF)
         lane = np.where((v & np.uint64(1)) == 1, y >> np.uint64(16), y & np.uint64(0xFFFF)).astype(np.int64)
         u = 0x3FFF - lane
