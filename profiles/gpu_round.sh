@@ -1,12 +1,11 @@
-# Round-end evidence on one B200: full GPU suite, smoke, default bench (with the
-# CPU baseline), reference arm, every named workload, the inference bench, the
-# warm launch list of a short bench run, and ncu --set full of the step kernels
-# and the preprocess kernels.  Outputs under gpurun_out/ (summaries: profiles/).
+# Round-end evidence on one B200, part A: full GPU suite, smoke, default bench
+# (with the CPU baseline), reference arm, every named workload, the inference
+# bench and the warm launch list of a short bench run.  Outputs in gpurun_out/.
 TAG="${1:-round}"
 set -x
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/smi_$TAG.txt
-timeout 1500 python -m pytest tests -q -m gpu --timeout 600 > gpurun_out/pytest_$TAG.log 2>&1; tail -3 gpurun_out/pytest_$TAG.log
+WJ_TRAIN_DROPOUT_REPORT=gpurun_out/train_dropout_$TAG.json timeout 1500 python -m pytest tests -q -m gpu --timeout 600 > gpurun_out/pytest_$TAG.log 2>&1; tail -3 gpurun_out/pytest_$TAG.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1; tail -1 gpurun_out/smoke_$TAG.log
 timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; head -c 300 gpurun_out/bench_$TAG.json; echo
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref_$TAG.json 2> gpurun_out/bench_ref_$TAG.err; head -c 300 gpurun_out/bench_ref_$TAG.json; echo
@@ -14,9 +13,6 @@ for c in c2 c1 c5b c5a c4; do
   timeout 400 python bench.py --config $c --no-cpu-baseline > gpurun_out/bench_${c}_$TAG.json 2> gpurun_out/bench_${c}_$TAG.err; echo "$c $(head -c 120 gpurun_out/bench_${c}_$TAG.json)"
 done
 timeout 600 python bench.py --what infer > gpurun_out/bench_infer_$TAG.json 2> gpurun_out/bench_infer_$TAG.err; head -c 300 gpurun_out/bench_infer_$TAG.json; echo
+timeout 600 python bench.py --what infer --impl reference --steps 2 --warmup 1 > gpurun_out/bench_infer_ref_$TAG.json 2> gpurun_out/bench_infer_ref_$TAG.err; head -c 300 gpurun_out/bench_infer_ref_$TAG.json; echo
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-epoch > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:join_encode -s 2 -c 1 -o gpurun_out/enc_$TAG -f python profiles/kernel_driver.py --config c3 --what chain --reps 4 > gpurun_out/ncu_enc_$TAG.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k "regex:tail_tc|adam" -s 2 -c 2 -o gpurun_out/tail_$TAG -f python profiles/kernel_driver.py --config c3 --what chain --reps 4 > gpurun_out/ncu_tail_$TAG.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:join_encode -s 2 -c 1 -o gpurun_out/score_$TAG -f python profiles/kernel_driver.py --config c3 --what score --reps 4 > gpurun_out/ncu_score_$TAG.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k "regex:rpe_kernel|sample_walks|intern|vindex|rpe_count" -o gpurun_out/pre_$TAG -f python profiles/kernel_driver.py --config c3 --what preprocess > gpurun_out/ncu_pre_$TAG.log 2>&1
 ls -la gpurun_out | tail -40
