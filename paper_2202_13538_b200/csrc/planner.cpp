@@ -124,7 +124,8 @@ struct HugeArray {
         size_t bytes = ((count * sizeof(T) + align - 1) / align) * align;
         ptr = static_cast<T *>(std::aligned_alloc(align, bytes ? bytes : align));
         if (!ptr) throw std::bad_alloc();
-        madvise(ptr, bytes, MADV_HUGEPAGE);
+        static const bool thp = !getenv("WJ_PLANNER_THP") || getenv("WJ_PLANNER_THP")[0] != '0';
+        if (thp) madvise(ptr, bytes, MADV_HUGEPAGE);
         n = count;
     }
     void fill(const T &v) { std::fill(ptr, ptr + n, v); }
@@ -366,7 +367,7 @@ extern "C" int wj_planner_create(const int64_t *positives, int64_t n_pos, int32_
                     if (i + D < hi) __builtin_prefetch(&p->filter1.slots[p->filter1.slot_of(key(i + D))], 1);
                     p->filter1.insert_atomic(key(i));
                 }
-            }, 1);
+            }, 3);  // cores left to the query-index thread and the caller (device preprocess)
         } else {
             p->filter2.reserve(n_filter);
             for (int64_t i = 0; i < n_filter; ++i) p->filter2.insert(pack2(filter_tuples + i * arity, arity));
