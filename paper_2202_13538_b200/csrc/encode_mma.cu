@@ -485,38 +485,8 @@ __global__ void __launch_bounds__(128) join_cross_kernel(const int64_t *__restri
     cp_async_wait_all();
     __syncthreads();
     pdl_trigger();
-    int32_t *out = cross + b * (int64_t)A * (A - 1) * mu;
-#pragma unroll
-    for (int a = 0; a < A; ++a)
-#pragma unroll
-        for (int j = a + 1; j < A; ++j) {
-            const int n0 = U[a], n1 = U[j], tot = n0 + n1;
-            const int32_t *X0 = sx + a * mu, *X1 = sx + j * mu, *I0 = sid + a * mu, *I1 = sid + j * mu;
-            int32_t *o0 = out + (a * (A - 1) + (j - 1)) * mu;  // list a relative to j (jj = j - 1 since j > a)
-            int32_t *o1 = out + (j * (A - 1) + a) * mu;        // list j relative to a (jj = a since a < j)
-            const int d0 = (int)(((int64_t)threadIdx.x * tot) / blockDim.x);
-            const int d1 = (int)(((int64_t)(threadIdx.x + 1) * tot) / blockDim.x);
-            int lo = max(0, d0 - n1), hi = min(d0, n0);
-            while (lo < hi) {  // merge-path split of diagonal d0 (ties: list a first)
-                const int mid = (lo + hi) >> 1;
-                if (X0[mid] <= X1[d0 - mid - 1])
-                    lo = mid + 1;
-                else
-                    hi = mid;
-            }
-            int i0 = lo, i1 = d0 - lo;
-            for (int d = d0; d < d1; ++d) {
-                const int32_t x0 = i0 < n0 ? X0[i0] : INT32_MAX;
-                const int32_t x1 = i1 < n1 ? X1[i1] : INT32_MAX;
-                if (i0 < n0 && x0 <= x1) {
-                    o0[i0] = x0 == x1 ? I1[i1] : 0;
-                    ++i0;
-                } else {
-                    o1[i1] = (i0 > 0 && X0[i0 - 1] == x1) ? I0[i0 - 1] : 0;
-                    ++i1;
-                }
-            }
-        }
+    // the same merge path as the join+encode kernel's prepass, into global memory
+    merge_cross<A>(threadIdx.x, blockDim.x, mu, sx, sid, U, cross + b * (int64_t)A * (A - 1) * mu);
 }
 
 template <int NW, int MINB, bool INF = false>

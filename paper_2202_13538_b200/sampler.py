@@ -201,8 +201,11 @@ def store_from_walks(walks: torch.Tensor, n: int, M: int, L: int, seed64: int, i
     _lib.call("wj_rpe_count", _lib.ptr(walks), n, M, L, n, _lib.ptr(counts), s)
     offsets = torch.zeros(n + 1, dtype=torch.int64, device=dev)
     torch.cumsum(counts, 0, out=offsets[1:])
-    total = int(offsets[-1].item())
-    max_unique = int(counts.max().item()) if n else 0
+    # one device -> host read for both sizes (the fill's allocation needs them)
+    if n:
+        total, max_unique = (int(v) for v in torch.stack([offsets[-1], counts.max().to(torch.int64)]).cpu())
+    else:
+        total, max_unique = 0, 0
     ux = torch.empty(total, dtype=torch.int32, device=dev)
     ukey = torch.empty(total, dtype=torch.int64, device=dev)
     ufirst = torch.empty(total, dtype=torch.int16, device=dev)
