@@ -233,6 +233,7 @@ class FusedScorer:
 
     def refresh(self) -> None:
         torch.cat([self.p.tensors[k].reshape(-1).to(torch.float32) for k in TENSOR_ORDER], out=self.flat)
+        self.version = getattr(self.p, "version", 0)
 
     def logits(self, q: torch.Tensor) -> torch.Tensor:
         """q [B, A] int64 on the store's device (ids already validated)."""

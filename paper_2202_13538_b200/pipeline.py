@@ -952,19 +952,23 @@ def _rows(queries) -> np.ndarray:
 
 
 def _check_ids(store: SubgraphStore, q: torch.Tensor) -> None:
-    """One range check of a device query batch (joiner.py:40-50)."""
-    if q.numel() and (int(q.min()) < 0 or int(q.max()) >= store.num_nodes):
-        raise ValueError(f"query node ids must lie in [0, {store.num_nodes})")
+    """One range check of a device query batch (joiner.py:40-50): min and max
+    in one reduction and one device-to-host read."""
+    if q.numel():
+        mn, mx = (int(v) for v in torch.stack(torch.aminmax(q)).cpu())
+        if mn < 0 or mx >= store.num_nodes:
+            raise ValueError(f"query node ids must lie in [0, {store.num_nodes})")
 
 
 def score_array(store: SubgraphStore, params: E.ModelParams, query_array, features=None,
-                chunk: int = 8192, validate: bool = True) -> torch.Tensor:
+                chunk: int = 1 << 16, validate: bool = True) -> torch.Tensor:
     """Sigmoid scores of a query array as a float64 DEVICE tensor
     (pipeline.py:185-198 without the host round trip).  RPE-only fp32 models
     inside the fused kernels' envelope score through wj_join_encode (keep = 1:
     no dropout stream, no backward statistics); feature models and other
     shapes through the dense join kernel + PyTorch encoder."""
-    q_all = torch.as_tensor(query_array, dtype=torch.int64).to(store.device)
+    q_all = torch.as_tensor(query_array, dtype=torch.int64)
+    q_all = q_all.to(store.device, non_blocking=q_all.device.type == "cpu" and q_all.is_pinned())
     if q_all.shape[0] == 0:
         return torch.empty(0, dtype=torch.float64, device=store.device)
     if q_all.dim() != 2 or q_all.shape[1] != params.arity:
@@ -974,7 +978,14 @@ def score_array(store: SubgraphStore, params: E.ModelParams, query_array, featur
     fused = features is None and E.fused_supported(params, store)
     scorer = None
     if fused and params.hidden == 64 and params.arity * store.width in E.TAIL_AW:
-        scorer = E.FusedScorer(params, store)  # join+encode (keep = 1) -> tail kernel
+        # join+encode (keep = 1) -> tail kernel; the scorer (buffers) is cached
+        # on the parameters, its flat copy of them refreshed on every call
+        scorer = getattr(params, "_scorer", None)
+        if scorer is None or scorer.store is not store:
+            scorer = E.FusedScorer(params, store)
+            params._scorer = scorer
+        else:
+            scorer.refresh()
     out = []
     for lo in range(0, q_all.shape[0], chunk):
         q = q_all[lo: lo + chunk]
