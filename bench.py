@@ -775,15 +775,24 @@ def run_ours_infer(args, cfg, store, ctx):
         barrier_sync()
     t_step = max_over_ranks(e0.elapsed_time(e1) / 1e3 / K)
     clk = clocks.summary()
-    # the join+encode kernel alone (keep = 1 variant)
+    # the scorer's join+encode kernel alone: wj_score_shared for runs of equal
+    # first anchors (this protocol), else the keep = 1 variant of wj_join_encode
     pooled = torch.empty((B, 64), device=dev)
     t = params.tensors
+    shared = scorer._use_shared(qd[0])
+
+    def enc(k):
+        if shared:
+            E.score_shared(store, qd[k], t["w1"], t["b1"], pooled)
+        else:
+            E.join_encode(store, qd[k], t["w1"], t["b1"], 1.0, 0, None, pooled)
+
     for k in range(W):
-        E.join_encode(store, qd[k], t["w1"], t["b1"], 1.0, 0, None, pooled)
+        enc(k)
     torch.cuda.synchronize()
     e0.record()
     for k in range(W, W + K):
-        E.join_encode(store, qd[k], t["w1"], t["b1"], 1.0, 0, None, pooled)
+        enc(k)
     e1.record()
     torch.cuda.synchronize()
     t_enc = e0.elapsed_time(e1) / 1e3 / K
@@ -803,7 +812,7 @@ def run_ours_infer(args, cfg, store, ctx):
     jb2 = join_bytes_q(cfg, ubar, 2)
     ach = jb2 * B / t_enc / 1e9
     cfg_name = [k for k, v in CONFIGS.items() if v is cfg][0]
-    ncu, fresh = ncu_capture(cfg_name, "wj_join_encode_infer")
+    ncu, fresh = ncu_capture(cfg_name, "wj_score_shared" if shared else "wj_join_encode_infer")
     out = {
         "metric": METRIC_INFER, "value": round(value, 1), "unit": "queries/s", "n_gpus": world, "steps": K,
         "warmup": W, "ms_per_step": round(t_step * 1e3, 4), "higher_is_better": True, "scaling": "weak",
@@ -818,16 +827,19 @@ def run_ours_infer(args, cfg, store, ctx):
                 "d2h_bytes_per_step": int(B * 8), "ms_per_step": round(t_e2e * 1e3, 4),
                 "path": "pinned host queries -> score_array (range check, H2D, join+encode keep=1, logits tail, "
                         "sigmoid) -> float64 scores to host, every step timed (wall clock, synchronised)"},
-        "roofline": {"kernel": "wj_join_encode keep = 1 variant (join + densify + layer 1, distinct landings)",
+        "roofline": {"kernel": ("wj_score_shared (join + densify + layer 1 at keep = 1, the shared first "
+                                "anchor's part once per run)" if shared else
+                                "wj_join_encode keep = 1 variant (join + densify + layer 1, distinct landings)"),
                      "bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "peak_kind": peak_kind,
                      "unit": "GB/s", "frac": round(ach / hbm, 4),
                      "traffic": (ncu or {}).get("dram_bytes_per_launch"),
-                     "traffic_source": (f"profiles/{cfg_name}_wj_join_encode_infer_ncu.json (same sources: "
-                                        f"{fresh})") if ncu else None,
+                     "traffic_source": (f"profiles/{cfg_name}_{'wj_score_shared' if shared else 'wj_join_encode_infer'}"
+                                        f"_ncu.json (same sources: {fresh})") if ncu else None,
                      "bytes_per_query": round(jb2, 1), "queries_per_launch": B,
                      "kernel_ms": round(t_enc * 1e3, 4), "kernel_share_of_step": round(t_enc / t_step, 3)},
         "gpu_launches": 2 * K,
-        "gpu_launches_note": "per timed step: wj_join_encode (keep = 1 variant) + wj_encoder_tail (logits)",
+        "gpu_launches_note": ("per timed step: " + ("wj_score_shared" if shared else "wj_join_encode (keep = 1 variant)")
+                              + " + wj_encoder_tail (logits)"),
         "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -232,6 +232,16 @@ int wj_adam(float *params, float *m, float *v, const float *partial, int32_t par
             int32_t n_params, float lr, float beta1, float beta2, float eps, const int64_t *step,
             float *grad_out, float *loss_out, wj_stream_t stream);
 
+/* Scoring of queries that share their first anchor (the test protocol: a
+ * positive followed by its negatives (u, v_i); pipeline.py:185-198): same
+ * pooled / S / msum as wj_join_encode at keep_prob = 1, bit for bit, with u's
+ * alone rows and their tile sums built once per run of equal first anchors
+ * in a CTA's contiguous range of queries.  Arity 2, hidden 64. */
+int wj_score_shared(const int64_t *queries, int64_t n_batch, const int64_t *offsets, const int32_t *uniq_x,
+                    const int32_t *uniq_id, const uint16_t *table_rows_f16, int32_t num_walks, int32_t num_steps,
+                    int32_t max_unique, const float *w1, const float *b1, float *pooled_out, float *s_out,
+                    float *msum_out, wj_stream_t stream);
+
 /* Step executor: one fused training step per wj_stepper_run -- replaces
  * the body of train()'s batch loop after the batch is drawn
  * (pipeline.py:302-305: _dense_batch -> forward -> bce_loss -> backward ->

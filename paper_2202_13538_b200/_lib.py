@@ -37,6 +37,7 @@ SIGNATURES = {
     "wj_join_encode": [P, I64, I32, P, P, P, P, P, P, P, P, I32, I32, I32, P, I64, P, P, I32, ctypes.c_float,
                        U64, P, P, P, P, P],
     "wj_join_cross": [P, I64, I32, P, P, P, I32, P, P],
+    "wj_score_shared": [P, I64, P, P, P, P, I32, I32, I32, P, P, P, P, P, P],
     "wj_vindex_count": [P, P, I64, P, I32, I32, P, P],
     "wj_vindex_fill": [P, P, I64, P, I32, I32, P, P, P, P],
     "wj_table_rows_f16": [P, I64, I32, I32, P, P],

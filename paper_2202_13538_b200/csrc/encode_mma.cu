@@ -489,6 +489,244 @@ __global__ void __launch_bounds__(128) join_cross_kernel(const int64_t *__restri
     merge_cross<A>(threadIdx.x, blockDim.x, mu, sx, sid, U, cross + b * (int64_t)A * (A - 1) * mu);
 }
 
+// ---------------------------------------------------------------------------
+// Scoring (keep = 1) of queries that share their first anchor -- the test
+// protocol: each positive (u, v) followed by its negatives (u, v_i)
+// (pipeline.py:185-198).  Same outputs as the keep = 1 variant
+// of join_encode_mma_kernel, organised around reuse: a CTA scores a
+// contiguous range of queries; for each new first anchor u it stages u's
+// sorted list once, writes u's "alone" rows [x_u | 0 | 1] (the rows of u's
+// landings that the second anchor's walks never reach) and sums their tiles
+// into S0(u).  Per query it stages only v's list, merges the two lists (cross
+// ids both ways), builds v's rows, and tiles v's landings plus every
+// co-reached landing of u twice: with its actual row (weight +2n) and its
+// alone row (weight -2n).  S^T and msum are integer sums, so S0(u) plus the
+// per-query tiles equal the full computation exactly; pooled is then formed
+// from S as in the join+encode kernel (bit-identical scores).
+constexpr int kCoCap = 128;  // co-reached landings of u per tile round (larger counts loop)
+
+template <int W>
+__device__ __forceinline__ uint16_t put_row2(const EncMmaArgs &g, unsigned char *xr, uint32_t row, int id0, int id1,
+                                             int own) {
+    uint32_t r[2][4];
+    const uint4 a = __ldg(g.trow + id0), b = __ldg(g.trow + id1);
+    r[0][0] = a.x, r[0][1] = a.y, r[0][2] = a.z, r[0][3] = a.w;
+    r[1][0] = b.x, r[1][1] = b.y, r[1][2] = b.z, r[1][3] = b.w;
+    uint32_t w[8];
+    splice_row<2, W>(r, w);
+    const uint32_t sw = (row >> 2) & 1u;
+    *reinterpret_cast<uint4 *>(xr + row * kRowB + (sw << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+    *reinterpret_cast<uint4 *>(xr + row * kRowB + ((sw ^ 1u) << 4)) = make_uint4(w[4], w[5], w[6], w[7]);
+    __half2 acc = __floats2half2_rn(0.f, 0.f);  // the own block's row sum n_l
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc = __hadd2(acc, *reinterpret_cast<const __half2 *>(&r[own][k]));
+    const __half n = __hadd(__low2half(acc), __high2half(acc));
+    return __half_as_ushort(__hadd(n, n));
+}
+
+template <int W>
+__global__ void __launch_bounds__(128, 3) infer_shared_kernel(EncMmaArgs g, int64_t per_cta) {
+    constexpr int A = 2, AW = 2 * W, H = 64, NT = 128, kMW = 4;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int mu = g.mu;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // W^T | rows [2 mu + kCoCap + 1] | S0 [64][kRedS] | sx, sid [2][mu] | scr [2][mu] | vl, nl | co
+    __half *wt = reinterpret_cast<__half *>(smem_raw);
+    unsigned char *xr = smem_raw + kWtBytes;  // u alone rows [0, mu), v rows [mu, 2mu), co rows, zero row
+    float *red = reinterpret_cast<float *>(xr + (size_t)mu * kRowB);  // over v / co rows (dead after tiles)
+    float *s0 = reinterpret_cast<float *>(xr + g.xr_bytes);
+    int32_t *sx = reinterpret_cast<int32_t *>(s0 + H * kRedS);
+    int32_t *sid = sx + 2 * mu;
+    int32_t *scr = sid + 2 * mu;
+    uint16_t *vl = reinterpret_cast<uint16_t *>(scr + 2 * mu);
+    uint16_t *nl = vl + g.lcap;
+    uint16_t *co = nl + g.lcap;
+    __shared__ int s_cnt, s_q[2], s_len[2];
+    __shared__ int64_t s_lo[2];
+    const uint32_t xr_s = smem_u32(xr), wt_s = smem_u32(wt);
+    const uint32_t zrow = (uint32_t)(2 * mu + kCoCap);
+    const int64_t b_lo = (int64_t)blockIdx.x * per_cta;
+    const int64_t b_hi = b_lo + per_cta < g.n_batch ? b_lo + per_cta : g.n_batch;
+    if (b_lo >= b_hi) return;
+    pdl_wait();
+    // ---- W1aug^T as a power-of-two-scaled fp16 hi + lo pair (as the join+encode kernel)
+    {
+        constexpr int PER = (H * 16 + NT - 1) / NT;
+        float wv[PER], mx = 0.f;
+        float *wred = s0;  // scratch before S0 is used
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int i = threadIdx.x + j * NT, m = i >> 4, k = i & 15;
+            wv[j] = (i >= H * 16) ? 0.f : (k < AW ? g.w1[k * H + m] : (k == AW ? g.b1[m] : 0.f));
+            mx = fmaxf(mx, fabsf(wv[j]));
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
+        if (lane == 0) wred[warp] = mx;
+        __syncthreads();
+        float m = 0.f;
+        for (int w = 0; w < kMW; ++w) m = fmaxf(m, wred[w]);
+        int e = 0;
+        if (m > 0.f) frexpf(m, &e);
+        const float sc = ldexpf(1.f, 14 - e);
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int i = threadIdx.x + j * NT, mm = i >> 4, k = i & 15;
+            if (i >= H * 16) break;
+            const float w = wv[j] * sc;
+            const __half hi = __float2half_rn(w);
+            const __half lo = __float2half_rn(w - __half2float(hi));
+            wt[mm * kWS + k] = hi;
+            wt[H * kWS + mm * kWS + k] = lo;
+        }
+        if (threadIdx.x < 2) *reinterpret_cast<uint4 *>(xr + zrow * kRowB + 16 * threadIdx.x) = make_uint4(0, 0, 0, 0);
+        __syncthreads();
+    }
+    pdl_trigger();
+    // tiles over vl[0, n) (padded to 16 with the zero row) into sacc
+    float sacc[4][2][4];
+    auto zero_acc = [&]() {
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int r = 0; r < 4; ++r) sacc[mt][nt][r] = 0.f;
+    };
+    auto run_tiles = [&](int n) {
+        const int np = (n + 15) & ~15;
+        for (int i = n + threadIdx.x; i < np; i += NT) {
+            vl[i] = (uint16_t)zrow;
+            nl[i] = 0;
+        }
+        __syncthreads();
+        for (int tt = warp; tt < (np >> 4); tt += kMW) {
+            const int v0 = tt << 4;
+            tile<0>(vl + v0, xr_s, wt_s, lane, 0u, 0u, 0u, sacc, reinterpret_cast<const uint32_t *>(nl + v0));
+        }
+    };
+    // per-warp S^T partials -> red (fixed order), returned for column c of unit m
+    auto reduce_to = [&](float *dst, bool add_s0) {
+        __syncthreads();
+        float *myred = red + warp * H * kRedS;
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const int c = 8 * nt + 2 * ((lane & 3)) + (r & 1);
+                    if (c <= AW) myred[(16 * mt + (lane >> 2) + 8 * (r >> 1)) * kRedS + c] = sacc[mt][nt][r];
+                }
+        __syncthreads();
+        if (threadIdx.x < H) {
+            const int m = threadIdx.x;
+            for (int c = 0; c <= AW; ++c) {
+                float s = add_s0 ? s0[m * kRedS + c] : 0.f;
+#pragma unroll
+                for (int w = 0; w < kMW; ++w) s += red[w * H * kRedS + m * kRedS + c];
+                dst[m * kRedS + c] = s;
+            }
+        }
+        __syncthreads();
+    };
+    float *outS = red;  // the final S^T of a query (written over red by reduce_to)
+    int cur_u = -1;
+    for (int64_t b = b_lo; b < b_hi; ++b) {
+        if (threadIdx.x < 2) {
+            const int64_t q = g.queries[b * 2 + threadIdx.x];
+            s_q[threadIdx.x] = (int)q;
+            s_lo[threadIdx.x] = g.offsets[q];
+            s_len[threadIdx.x] = (int)(g.offsets[q + 1] - g.offsets[q]);
+        }
+        __syncthreads();
+        const int U[2] = {s_len[0], s_len[1]};
+        if (s_q[0] != cur_u) {  // ---- u's list, alone rows and S0(u), once per first anchor
+            for (int i = threadIdx.x; i < U[0]; i += NT) {
+                cp_async4(sx + i, g.ux + s_lo[0] + i);
+                cp_async4(sid + i, g.uid + s_lo[0] + i);
+            }
+            cp_async_wait_all();
+            __syncthreads();
+            for (int l = threadIdx.x; l < U[0]; l += NT) {
+                nl[l] = put_row2<W>(g, xr, (uint32_t)l, sid[l], 0, 0);
+                vl[l] = (uint16_t)l;
+            }
+            zero_acc();
+            run_tiles(U[0]);
+            reduce_to(s0, false);
+            cur_u = s_q[0];
+        }
+        // ---- v: stage, merge (cross ids both ways), rows
+        for (int i = threadIdx.x; i < U[1]; i += NT) {
+            cp_async4(sx + mu + i, g.ux + s_lo[1] + i);
+            cp_async4(sid + mu + i, g.uid + s_lo[1] + i);
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        merge_cross<2>(threadIdx.x, NT, mu, sx, sid, U, scr);
+        __syncthreads();
+        // v's rows [counts rel. u (cross) | counts rel. v (own) | 1], weight 2 n_l
+        for (int l = threadIdx.x; l < U[1]; l += NT) {
+            nl[l] = put_row2<W>(g, xr, (uint32_t)(mu + l), scr[mu + l], sid[mu + l], 1);
+            vl[l] = (uint16_t)(mu + l);
+        }
+        zero_acc();
+        int nv = U[1];
+        // co-reached landings of u (cross id rel. v != 0): rounds of whole
+        // strides of NT landings, at most kCoCap (>= NT) per round; each round
+        // tiles their actual rows (+2n) and their alone rows (-2n)
+        int start = 0;
+        while (true) {
+            int nco = 0, l0 = start;
+            while (l0 < U[0]) {
+                if (threadIdx.x == 0) s_cnt = 0;
+                __syncthreads();  // also: the previous round's tiles are done
+                const int l = l0 + threadIdx.x;
+                const bool hit = l < U[0] && scr[l] != 0;
+                const unsigned bm = __ballot_sync(kFull, hit);
+                int wb = 0;
+                if (lane == 0 && bm) wb = atomicAdd(&s_cnt, __popc(bm));
+                __syncthreads();
+                const int h = s_cnt;
+                if (nco + h > kCoCap) break;  // uniform; this stride opens the next round
+                wb = __shfl_sync(kFull, wb, 0);
+                if (hit) co[nco + wb + __popc(bm & lanemask_lt())] = (uint16_t)l;
+                nco += h;
+                l0 += NT;
+            }
+            start = l0;
+            __syncthreads();
+            for (int k = threadIdx.x; k < nco; k += NT) {
+                const int l = co[k];
+                const uint16_t n2 = put_row2<W>(g, xr, (uint32_t)(2 * mu + k), sid[l], scr[l], 0);
+                vl[nv + k] = (uint16_t)(2 * mu + k);
+                nl[nv + k] = n2;
+                vl[nv + nco + k] = (uint16_t)l;
+                nl[nv + nco + k] = (uint16_t)(n2 ^ 0x8000u);  // -2 n_l
+            }
+            run_tiles(nv + 2 * nco);
+            nv = 0;
+            if (start >= U[0]) break;
+        }
+        reduce_to(outS, true);
+        if (threadIdx.x < H) {
+            const int m = threadIdx.x;
+            float sv[AW + 1];
+#pragma unroll
+            for (int c = 0; c <= AW; ++c) sv[c] = outS[m * kRedS + c] * 0.5f;
+            float pv = g.b1[m] * sv[AW];
+#pragma unroll
+            for (int c = 0; c < AW; ++c) pv = fmaf(g.w1[c * H + m], sv[c], pv);
+            g.pooled[b * H + m] = pv;
+            if (g.s_out)
+                for (int c = 0; c < AW; ++c) g.s_out[(b * AW + c) * (int64_t)H + m] = sv[c];
+            if (g.msum) g.msum[b * H + m] = sv[AW];
+        }
+        __syncthreads();
+    }
+}
+
 template <int NW, int MINB, bool INF = false>
 static EncMmaKernel pick_mma(int A, int W) {
 #define WJ_CASE(a, w) \
@@ -705,6 +943,83 @@ extern "C" int wj_join_encode(const int64_t *queries, int64_t n_batch, int32_t a
     return check_launch("wj_join_encode");
 }
 
+
+// Scoring of queries that share their first anchor (infer_shared_kernel):
+// pooled [B, 64] (and S / msum when given) exactly as wj_join_encode at
+// keep = 1.  Arity 2, hidden 64, A (L+1) + 1 <= 16.
+extern "C" int wj_score_shared(const int64_t *queries, int64_t n_batch, const int64_t *offsets,
+                               const int32_t *uniq_x, const int32_t *uniq_id, const uint16_t *table_rows_f16,
+                               int32_t num_walks, int32_t num_steps, int32_t max_unique, const float *w1,
+                               const float *b1, float *pooled_out, float *s_out, float *msum_out,
+                               wj_stream_t stream) {
+    using namespace wj;
+    const int W = num_steps + 1;
+    if (!queries || !offsets || !uniq_x || !uniq_id || !table_rows_f16 || !w1 || !b1 || !pooled_out ||
+        num_walks < 1 || num_steps < 1 || max_unique < 1) {
+        set_error("wj_score_shared: bad arguments");
+        return WJ_ERR_ARG;
+    }
+    if (2 * W + 1 > 16 || 2 * (int64_t)max_unique + kCoCap + 1 > 65535) {
+        set_error("wj_score_shared: shape outside the kernel (A(L+1)+1 <= 16, rows < 65536)");
+        return WJ_ERR_UNSUPPORTED;
+    }
+    if (n_batch == 0) return WJ_OK;
+    using K = void (*)(EncMmaArgs, int64_t);
+    K k = nullptr;
+    switch (W) {
+        case 2: k = infer_shared_kernel<2>; break;
+        case 3: k = infer_shared_kernel<3>; break;
+        case 4: k = infer_shared_kernel<4>; break;
+        case 5: k = infer_shared_kernel<5>; break;
+        case 6: k = infer_shared_kernel<6>; break;
+        case 7: k = infer_shared_kernel<7>; break;
+        default: break;
+    }
+    if (!k) {
+        set_error("wj_score_shared: L+1 = %d not instantiated", W);
+        return WJ_ERR_UNSUPPORTED;
+    }
+    const int mu = max_unique;
+    EncMmaArgs g = EncMmaArgs{};
+    g.queries = queries;
+    g.n_batch = n_batch;
+    g.offsets = offsets;
+    g.ux = uniq_x;
+    g.uid = uniq_id;
+    g.trow = reinterpret_cast<const uint4 *>(table_rows_f16);
+    g.mu = mu;
+    g.lcap = (mu + 2 * kCoCap + 32 + 7) & ~7;
+    const int64_t rows_b = (int64_t)(2 * mu + kCoCap + 1) * kRowB;
+    const int64_t red_b = (int64_t)mu * kRowB + 4 * 64 * kRedS * 4;
+    g.xr_bytes = (int)(((rows_b > red_b ? rows_b : red_b) + 15) & ~15LL);
+    g.w1 = w1;
+    g.b1 = b1;
+    g.pooled = pooled_out;
+    g.s_out = s_out;
+    g.msum = msum_out;
+    const size_t smem = (size_t)kWtBytes + g.xr_bytes + 64 * kRedS * 4 + (size_t)6 * mu * 4 + (size_t)g.lcap * 4 +
+                        kCoCap * 2;
+    if (smem > 227 * 1024) {
+        set_error("wj_score_shared needs %zu B of shared memory", smem);
+        return WJ_ERR_UNSUPPORTED;
+    }
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) {
+        set_error("wj_score_shared smem attribute: %s", cudaGetErrorString(e));
+        return WJ_ERR_CUDA;
+    }
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 128, smem);
+    const int64_t slots = (int64_t)sm_count() * (per_sm > 0 ? per_sm : 1);
+    const int64_t per_cta = (n_batch + slots - 1) / slots;
+    const int64_t blocks = (n_batch + per_cta - 1) / per_cta;
+    e = launch_pdl(k, dim3((unsigned)blocks), dim3(128), smem, (cudaStream_t)stream, g, per_cta);
+    if (e != cudaSuccess) {
+        set_error("wj_score_shared launch: %s", cudaGetErrorString(e));
+        return WJ_ERR_CUDA;
+    }
+    return check_launch("wj_score_shared");
+}
 
 // ---------------------------------------------------------------------------
 // Step executor: one fused training step (wj_join_encode -> wj_encoder_tail

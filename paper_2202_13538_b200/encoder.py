@@ -181,6 +181,19 @@ def join_encode(store, q: torch.Tensor, w1: torch.Tensor, b1: torch.Tensor, keep
         _lib.call("wj_join_encode", *args, _lib.ptr(cross), *store.vindex_ptrs(), *tail)
 
 
+def score_shared(store, q: torch.Tensor, w1: torch.Tensor, b1: torch.Tensor, pooled: torch.Tensor,
+                 S: Optional[torch.Tensor] = None, msum: Optional[torch.Tensor] = None) -> None:
+    """One wj_score_shared launch: keep = 1 scoring of a batch whose queries
+    come in runs of equal first anchors (a positive and its negatives); the
+    same pooled / S / msum as ``join_encode(..., keep=1.0)``, bit for bit."""
+    from . import _lib
+
+    _lib.call("wj_score_shared", _lib.ptr(q), q.shape[0], _lib.ptr(store.offsets_d), _lib.ptr(store.uniq_x_d),
+              _lib.ptr(store.uniq_id_d), _lib.ptr(store.trow_d), store.num_walks, store.walk_steps,
+              store.max_unique, _lib.ptr(w1), _lib.ptr(b1), _lib.ptr(pooled), _lib.ptr(S), _lib.ptr(msum),
+              _lib.stream_handle(store.device))
+
+
 def fused_supported(p: ModelParams, store) -> bool:
     """True when wj_join_encode (tensor-core or SIMT kernel) accepts this
     model / store shape: RPE-only fp32 models whose (arity, L+1, hidden,
@@ -231,6 +244,21 @@ class FusedScorer:
         self.refresh()
         self._bufs = {}
 
+    def _use_shared(self, q: torch.Tensor) -> bool:
+        """wj_score_shared when the queries come in long runs of equal first
+        anchors (arity 2, L + 1 <= 7; WJ_SCORE_SHARED=0/1 forces it off / on)."""
+        import os
+
+        env = os.environ.get("WJ_SCORE_SHARED")
+        ok = q.shape[1] == 2 and self.store.width <= 7 and self.store.trow_d is not None
+        if env is not None:
+            return env == "1" and ok
+        B = q.shape[0]
+        if not ok or B < 1024:
+            return False
+        runs = 1 + int((q[1:, 0] != q[:-1, 0]).sum())
+        return runs * 32 <= B
+
     def refresh(self) -> None:
         torch.cat([self.p.tensors[k].reshape(-1).to(torch.float32) for k in TENSOR_ORDER], out=self.flat)
         self.version = getattr(self.p, "version", 0)
@@ -248,7 +276,10 @@ class FusedScorer:
             self._bufs = {B: buf}
         pooled, logits = buf
         t = self.p.tensors
-        join_encode(self.store, q, t["w1"], t["b1"], 1.0, 0, None, pooled)
+        if self._use_shared(q):  # runs of equal first anchors: u's part once per run
+            score_shared(self.store, q, t["w1"], t["b1"], pooled)
+        else:
+            join_encode(self.store, q, t["w1"], t["b1"], 1.0, 0, None, pooled)
         scale = 1.0 / (A * self.store.landings)
         _lib.call("wj_encoder_tail", _lib.ptr(pooled), None, None, None, B, A * self.store.width, 64,
                   _lib.ptr(self.flat), self.offs_c, scale, _lib.ptr(logits), None, 0, None, None,
