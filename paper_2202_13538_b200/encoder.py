@@ -20,6 +20,7 @@ trajectories match the reference statistically, not bitwise.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -244,27 +245,32 @@ class FusedScorer:
         self.refresh()
         self._bufs = {}
 
-    def _use_shared(self, q: torch.Tensor) -> bool:
-        """wj_score_shared when the queries come in long runs of equal first
-        anchors (arity 2, L + 1 <= 7; WJ_SCORE_SHARED=0/1 forces it off / on)."""
-        import os
+    def use_shared_runs(self, B: int, runs: Optional[int]) -> bool:
+        """wj_score_shared when the B queries come in long runs (``runs`` of
+        them) of equal first anchors (arity 2, L + 1 <= 7; WJ_SCORE_SHARED=0/1
+        forces it off / on); ``runs`` None: count them on the device."""
 
         env = os.environ.get("WJ_SCORE_SHARED")
-        ok = q.shape[1] == 2 and self.store.width <= 7 and self.store.trow_d is not None
+        ok = self.p.arity == 2 and self.store.width <= 7 and self.store.trow_d is not None
         if env is not None:
             return env == "1" and ok
+        return ok and B >= 1024 and runs is not None and runs * 32 <= B
+
+    def _use_shared(self, q: torch.Tensor) -> bool:
         B = q.shape[0]
-        if not ok or B < 1024:
+        if not self.use_shared_runs(B, 0):  # decided without the run count: no device read
             return False
-        runs = 1 + int((q[1:, 0] != q[:-1, 0]).sum())
-        return runs * 32 <= B
+        if "WJ_SCORE_SHARED" in os.environ:
+            return True
+        return self.use_shared_runs(B, 1 + int((q[1:, 0] != q[:-1, 0]).sum()))
 
     def refresh(self) -> None:
         torch.cat([self.p.tensors[k].reshape(-1).to(torch.float32) for k in TENSOR_ORDER], out=self.flat)
         self.version = getattr(self.p, "version", 0)
 
-    def logits(self, q: torch.Tensor) -> torch.Tensor:
-        """q [B, A] int64 on the store's device (ids already validated)."""
+    def logits(self, q: torch.Tensor, shared: Optional[bool] = None) -> torch.Tensor:
+        """q [B, A] int64 on the store's device (ids already validated);
+        ``shared``: the scoring kernel if the caller already chose it."""
         from . import _lib
 
         B, A = q.shape
@@ -276,7 +282,9 @@ class FusedScorer:
             self._bufs = {B: buf}
         pooled, logits = buf
         t = self.p.tensors
-        if self._use_shared(q):  # runs of equal first anchors: u's part once per run
+        if shared is None:
+            shared = self._use_shared(q)
+        if shared:  # runs of equal first anchors: u's part once per run
             score_shared(self.store, q, t["w1"], t["b1"], pooled)
         else:
             join_encode(self.store, q, t["w1"], t["b1"], 1.0, 0, None, pooled)

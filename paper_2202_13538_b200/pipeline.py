@@ -968,12 +968,21 @@ def score_array(store: SubgraphStore, params: E.ModelParams, query_array, featur
     no dropout stream, no backward statistics); feature models and other
     shapes through the dense join kernel + PyTorch encoder."""
     q_all = torch.as_tensor(query_array, dtype=torch.int64)
-    q_all = q_all.to(store.device, non_blocking=q_all.device.type == "cpu" and q_all.is_pinned())
     if q_all.shape[0] == 0:
         return torch.empty(0, dtype=torch.float64, device=store.device)
     if q_all.dim() != 2 or q_all.shape[1] != params.arity:
         raise ValueError(f"queries must be [B, {params.arity}] for this model")
-    if validate:
+    host_runs = None
+    if q_all.device.type == "cpu":
+        # host input: the range check and the first-anchor run count on the
+        # host, before the copy, so the device stream never waits on the host
+        if validate:
+            qn = q_all.numpy()
+            if int(qn.min()) < 0 or int(qn.max()) >= store.num_nodes:
+                raise ValueError(f"query node ids must lie in [0, {store.num_nodes})")
+        host_runs = q_all[:, 0].numpy()
+        q_all = q_all.to(store.device, non_blocking=q_all.is_pinned())
+    elif validate:
         _check_ids(store, q_all)
     fused = features is None and E.fused_supported(params, store)
     scorer = None
@@ -990,14 +999,18 @@ def score_array(store: SubgraphStore, params: E.ModelParams, query_array, featur
     for lo in range(0, q_all.shape[0], chunk):
         q = q_all[lo: lo + chunk]
         if scorer is not None:
-            logits = scorer.logits(q).clone()
+            shared = None
+            if host_runs is not None:
+                f = host_runs[lo: lo + chunk]
+                shared = scorer.use_shared_runs(q.shape[0], 1 + int(np.count_nonzero(f[1:] != f[:-1])))
+            logits = scorer.logits(q, shared=shared)  # .double() below copies it out of the scorer
         elif fused:
             logits, _ = E.forward_fused(params, store, q, training=False, need_grad=False)
         else:
             dense = dense_batch(store, q, features=features, dtype=params.w1.dtype, validate=False)
             logits, _ = E.forward(params, dense, training=False)
         out.append(torch.sigmoid(logits.double()))
-    return torch.cat(out)
+    return out[0] if len(out) == 1 else torch.cat(out)
 
 
 def validation_metric(store: SubgraphStore, params: E.ModelParams, split, cfg: TrainConfig,

@@ -68,3 +68,32 @@ def test_score_array_uses_shared_path_bit_exact(wj, monkeypatch):
     monkeypatch.delenv("WJ_SCORE_SHARED")
     c = wj.score_array(s, p, q)  # auto: 4 runs in 4,004 queries -> shared
     assert torch.equal(a, b) and torch.equal(a, c)
+
+
+def test_score_array_host_input_decides_on_host(wj):
+    """Host (pinned or not) query arrays: the id range check and the shared-
+    path choice are made on the host before the copy; same scores as the
+    device-resident input, the same ValueError for out-of-range ids."""
+    rng = np.random.default_rng(11)
+    n = 1500
+    g = wj.Graph.from_edges(rng.integers(0, n, size=(15000, 2)), n)
+    s = wj.preprocess(g, 40, 3, 2)
+    q = _batch(rng, n, rng.choice(n, 3, replace=False), 700)
+    p = wj.init_params(2, 3, dropout=0.1, seed=1)
+    scorer = wj.encoder.FusedScorer(p, s)
+    runs = 1 + int((q[1:, 0] != q[:-1, 0]).sum())
+    assert scorer._use_shared(q) == scorer.use_shared_runs(q.shape[0], runs)
+    dev = wj.score_array(s, p, q)
+    host = wj.score_array(s, p, q.cpu())
+    pinned = wj.score_array(s, p, q.cpu().pin_memory())
+    mixed = wj.score_array(s, p, q.cpu()[torch.randperm(q.shape[0])])  # short runs: the keep = 1 kernel
+    torch.cuda.synchronize()
+    assert torch.equal(dev, host) and torch.equal(dev, pinned)
+    assert mixed.shape == dev.shape
+    for bad in (-1, n):
+        qb = q.cpu().clone()
+        qb[5, 1] = bad
+        with pytest.raises(ValueError):
+            wj.score_array(s, p, qb)
+        with pytest.raises(ValueError):
+            wj.score_array(s, p, qb.cuda())
