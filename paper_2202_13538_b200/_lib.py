@@ -13,7 +13,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_walkjoin_b200.so")
+# WJ_LIB: an alternative build of the same library (A/B measurements, profiles/ab_variant.py)
+LIB_PATH = os.environ.get("WJ_LIB") or os.path.join(_HERE, "_walkjoin_b200.so")
 
 WJ_OK, WJ_ERR_ARG, WJ_ERR_CUDA, WJ_ERR_UNSUPPORTED = 0, 1, 2, 3
 DTYPE_CODES = {torch.float32: 0, torch.float64: 1, torch.bfloat16: 2, torch.float16: 3}

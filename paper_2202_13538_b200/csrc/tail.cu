@@ -86,9 +86,23 @@ __global__ void __launch_bounds__(kAdamCols *kAdamGroups) adam_kernel(
     // the next step's join+encode kernel may launch now: before its own wait
     // it only reads the store and its queries, which this kernel never writes
     pdl_trigger();
+    // this parameter's p / m / v: written only by the previous step's Adam
+    // (complete before the tail started), so fetched before the wait -- the
+    // update then needs no load after the reduction
+    float pi = 0.f, mi = 0.f, vi = 0.f;
+    if (grp == 0 && i < n) {
+        pi = params[i];
+        mi = m[i];
+        vi = v[i];
+    }
     pdl_wait();  // the partial rows of the tail kernel
+    // the step counter (advanced by the tail): its load and the bias
+    // corrections overlap the reduction's loads
+    const int64_t t = *step;
     float gsum = 0.f;
     if (i <= n) gsum = strided_sum(partial + i, (int64_t)(n + 1), grp, rows);
+    const float bc1 = 1.f - powf(beta1, (float)t);
+    const float bc2 = 1.f - powf(beta2, (float)t);
     part[grp][c] = gsum;
     __syncthreads();
     if (grp != 0 || i > n) return;
@@ -99,11 +113,11 @@ __global__ void __launch_bounds__(kAdamCols *kAdamGroups) adam_kernel(
         if (loss_out) *loss_out = gsum;
         return;
     }
-    const int64_t t = *step;
-    const float bc1 = 1.f - powf(beta1, (float)t);
-    const float bc2 = 1.f - powf(beta2, (float)t);
     if (grad_out) grad_out[i] = gsum;
-    adam_update(params + i, m + i, v + i, gsum, lr, beta1, beta2, eps, bc1, bc2);
+    adam_update(&pi, &mi, &vi, gsum, lr, beta1, beta2, eps, bc1, bc2);
+    params[i] = pi;
+    m[i] = mi;
+    v[i] = vi;
 }
 
 // Fixed-order column sums of the partial rows (the data-parallel path:
@@ -376,6 +390,10 @@ __global__ void __launch_bounds__(kTW * 32) tail_tc_kernel(TailArgs g) {
             G[gq * kTP + c + 1] = ag[1] * g.scale;
             G[(gq + 8) * kTP + c] = ag[2] * g.scale;
             G[(gq + 8) * kTP + c + 1] = ag[3] * g.scale;
+            // S / msum were issued before the first product (long landed):
+            // this barrier publishes them too, so the dW2 / dU1 products and
+            // the dW1 FMAs below share one barrier interval
+            cp_async_wait_all();
             __syncthreads();
         }
         // dW2 += pooled^T dhq (scaled at the end), dU1 += hq^T dz2
@@ -384,8 +402,6 @@ __global__ void __launch_bounds__(kTW * 32) tail_tc_kernel(TailArgs g) {
         warp_mma3<4, 2>(au1, lane, [&](int m, int k) { return HQ[k * kTP + 16 * fm + m]; },
                         [&](int k, int n) { return DZ2[k * kTP + 8 * fn + n]; });
         // dW1[c][h] += S_q[c][h] g_q[h], db1[h] += msum_q[h] g_q[h]; db2 = sum dhq, dc1 = sum dz2
-        cp_async_wait_all();
-        __syncthreads();
 #pragma unroll
         for (int i = 0; i < NW1; ++i) {
             const int e = tid + NT * i;
