@@ -411,6 +411,14 @@ int wj_train_epoch(wj_stepper *stepper, wj_planner *planner, const int64_t *ring
                    const float *dev_labels, float *loss_out, int64_t max_steps, wj_stream_t stream,
                    wj_stream_t copy_stream, int64_t *steps_done, int64_t *h2d_bytes);
 
+/* Host -> device copy of a large pageable host array (the graph CSR of a
+ * host-input preprocess; replaces the torch/driver pageable copy inside
+ * reference-facing sampler.preprocess(graph) -> sampler.py:94-151): the
+ * array is split over `threads` workers, each staging its part through its
+ * own pinned double buffer on its own stream.  Synchronous: every byte is on
+ * the device when it returns. */
+int wj_upload(void *dst, const void *src, int64_t bytes, int32_t threads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -63,6 +63,7 @@ SIGNATURES = {
     "wj_surl_pack": [P, I64, I32, P, P, P, P, P, P],
     "wj_surl_unpack": [P, I64, I32, P, P, P, P, P, P],
     "wj_planner_create": [P, I64, I32, P, I64, I64, I32, I32, I32, P, I64, P],
+    "wj_upload": [P, P, I64, I32],
     "wj_planner_destroy": [P],
     "wj_planner_set_rng": [P, P],
     "wj_planner_get_rng": [P, P],

@@ -14,7 +14,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "_walkjoin_b200.so")
 SOURCES = ["capi.cu", "sampler.cu", "rpe.cu", "intern.cu", "join.cu", "encode.cu", "encode_mma.cu", "encode_tc.cu", "tail.cu",
-           "vindex.cu", "surl.cu", "planner.cpp", "epoch.cu"]
+           "vindex.cu", "surl.cu", "planner.cpp", "epoch.cu", "upload.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-O3", "-std=c++17", "-lineinfo", "--use_fast_math",

@@ -177,6 +177,35 @@ def project_hyperedges(lines: Iterable[str]) -> Graph:
 
 # ----------------------------------------------------------------- device --
 
+_UPLOAD_MIN = 16 << 20  # below this a plain copy is as fast
+
+
+def upload(arr: np.ndarray, device) -> torch.Tensor:
+    """Contiguous host array -> new device tensor.  Large arrays go through
+    wj_upload (several host threads staging through pinned buffers, ~4x the
+    driver's single-threaded pageable copy); the call returns with the data
+    on the device."""
+    import os
+
+    from . import _lib
+
+    arr = np.ascontiguousarray(arr)
+    device = torch.device(device)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", UserWarning)  # non-writable numpy view: only read
+        src = torch.from_numpy(arr)
+    if device.type != "cuda" or arr.nbytes < _UPLOAD_MIN:
+        return src.to(device)
+    out = torch.empty(arr.shape, dtype=src.dtype, device=device)
+    with torch.cuda.device(device):
+        # the new block may have been freed by work still queued on this
+        # stream; wj_upload writes from its own streams
+        torch.cuda.current_stream(device).synchronize()
+        threads = max(1, min(8, (os.cpu_count() or 2) // 2))
+        _lib.call("wj_upload", out.data_ptr(), arr.ctypes.data, arr.nbytes, threads)
+    return out
+
+
 class DeviceGraph:
     """CSR resident in HBM: int32 idxptr when 2E < 2^31, int32 indices."""
 
@@ -204,10 +233,7 @@ class DeviceGraph:
         # no host-side copy of the (large) indices array when it is already
         # contiguous int32; read-only arrays are fine for the H2D copy
         ix = np.ascontiguousarray(np.asarray(g.indices), dtype=np.int32)
-        with warnings.catch_warnings():
-            warnings.simplefilter("ignore", UserWarning)  # non-writable numpy view: torch only reads it
-            ipt, ixt = torch.from_numpy(ip), torch.from_numpy(ix)
-        return cls(n, ipt.to(device), ixt.to(device), getattr(g, "id_map", None))
+        return cls(n, upload(ip, device), upload(ix, device), getattr(g, "id_map", None))
 
     def to_host(self) -> Graph:
         return Graph(self.num_nodes, self.idxptr.cpu().numpy().astype(np.int64),

@@ -164,3 +164,22 @@ def test_eager_adam_bias_corrections_from_device_counter(wj):
     for k in res[0]:
         torch.testing.assert_close(res[0][k], res[2][k], rtol=1e-5, atol=1e-6)
         torch.testing.assert_close(res[1][k], res[2][k], rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.parametrize("nbytes", [3, 17 << 20, (40 << 20) + 12, (130 << 20) + 4])
+def test_upload_is_an_exact_copy(wj, nbytes):
+    """wj_upload (multi-threaded pinned staging of the host CSR) == the host
+    bytes, for sizes below, at and across its chunking."""
+    from paper_2202_13538_b200.graph import upload
+
+    rng = np.random.default_rng(nbytes)
+    host = rng.integers(0, 256, size=nbytes, dtype=np.uint8)
+    dev = upload(host, "cuda:0")
+    assert dev.device.type == "cuda" and dev.dtype == torch.uint8
+    assert np.array_equal(dev.cpu().numpy(), host)
+    # through the C-ABI directly, into an int32 view with an odd element count
+    h32 = rng.integers(-2**31, 2**31 - 1, size=(nbytes // 4) or 1, dtype=np.int32)
+    d32 = torch.empty(h32.shape, dtype=torch.int32, device="cuda:0")
+    torch.cuda.synchronize()
+    wj._lib.call("wj_upload", d32.data_ptr(), h32.ctypes.data, h32.nbytes, 5)
+    assert np.array_equal(d32.cpu().numpy(), h32)
