@@ -66,6 +66,31 @@ __device__ __forceinline__ void adam_update(float *p, float *m, float *v, float 
 // chains (four loads in flight), combined in a fixed order
 __device__ __forceinline__ float strided_sum(const float *p, int64_t ld, int grp, int rows) {
     float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    if (rows <= 16 * kAdamGroups) {
+        // every load of the thread in flight at once (one L2 round trip, not
+        // one per four rows), then the same additions in the same order
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int r = grp + kAdamGroups * i;
+            v[i] = r < rows ? p[(int64_t)r * ld] : 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int r = grp + 4 * kAdamGroups * k;
+            if (r + 3 * kAdamGroups < rows) {  // a full group of four: one per chain
+                s0 += v[4 * k];
+                s1 += v[4 * k + 1];
+                s2 += v[4 * k + 2];
+                s3 += v[4 * k + 3];
+            } else {  // the remainder rows, all into chain 0
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (r + kAdamGroups * j < rows) s0 += v[4 * k + j];
+            }
+        }
+        return (s0 + s1) + (s2 + s3);
+    }
     int r = grp;
     for (; r + 3 * kAdamGroups < rows; r += 4 * kAdamGroups) {
         s0 += p[(int64_t)r * ld];
