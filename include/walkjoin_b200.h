@@ -215,7 +215,8 @@ int wj_join_encode_simt(const int64_t *queries, int64_t n_batch, int32_t arity,
  * NULL) gets the [B] logits.  Training (labels != NULL) launches exactly
  * partial_rows CTAs: CTA i reduces queries [i*q, (i+1)*q), q = ceil(B /
  * partial_rows) (best: partial_rows = ceil(B / 16)), in a fixed order into
- * partial[i, 0:total] and its loss partial into partial[i, total].  work is
+ * partial[i, 0:total] and its loss partial into partial[i, total] (partial
+ * 8-byte aligned: rows are written with 8-B stores).  work is
  * unused (may be NULL).  step_inc (nullable) is incremented by one when the
  * tail is done (the graph-resident step counter wj_join_encode and wj_adam
  * read).  The [16 x 64] x [64 x 64] products run on the tensor cores in

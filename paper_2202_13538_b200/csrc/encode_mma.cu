@@ -541,7 +541,11 @@ __global__ void __launch_bounds__(128, 3) infer_shared_kernel(EncMmaArgs g, int6
     uint16_t *vl = reinterpret_cast<uint16_t *>(scr + 2 * mu);
     uint16_t *nl = vl + g.lcap;
     uint16_t *co = nl + g.lcap;
-    __shared__ int s_cnt, s_q[2], s_len[2];
+    // co-reached counter, triple-buffered: iteration i counts into s_cnt[i % 3]
+    // and resets s_cnt[(i + 1) % 3], whose last readers (iteration i - 2)
+    // all passed iteration i - 1's barrier -- a single counter reset at the
+    // top of the next iteration raced with slow warps still reading it
+    __shared__ int s_cnt[3], s_q[2], s_len[2];
     __shared__ int64_t s_lo[2];
     const uint32_t xr_s = smem_u32(xr), wt_s = smem_u32(wt);
     const uint32_t zrow = (uint32_t)(2 * mu + kCoCap);
@@ -580,9 +584,11 @@ __global__ void __launch_bounds__(128, 3) infer_shared_kernel(EncMmaArgs g, int6
             wt[H * kWS + mm * kWS + k] = lo;
         }
         if (threadIdx.x < 2) *reinterpret_cast<uint4 *>(xr + zrow * kRowB + 16 * threadIdx.x) = make_uint4(0, 0, 0, 0);
+        if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
         __syncthreads();
     }
     pdl_trigger();
+    int ci = 0;  // co-reached counter iteration (uniform)
     // tiles over vl[0, n) (padded to 16 with the zero row) into sacc
     float sacc[4][2][4];
     auto zero_acc = [&]() {
@@ -680,15 +686,17 @@ __global__ void __launch_bounds__(128, 3) infer_shared_kernel(EncMmaArgs g, int6
         while (true) {
             int nco = 0, l0 = start;
             while (l0 < U[0]) {
-                if (threadIdx.x == 0) s_cnt = 0;
-                __syncthreads();  // also: the previous round's tiles are done
+                const int cs = ci % 3;
+                __syncthreads();  // the previous round's tiles are done
                 const int l = l0 + threadIdx.x;
                 const bool hit = l < U[0] && scr[l] != 0;
                 const unsigned bm = __ballot_sync(kFull, hit);
                 int wb = 0;
-                if (lane == 0 && bm) wb = atomicAdd(&s_cnt, __popc(bm));
+                if (lane == 0 && bm) wb = atomicAdd(&s_cnt[cs], __popc(bm));
+                if (threadIdx.x == 0) s_cnt[(ci + 1) % 3] = 0;
                 __syncthreads();
-                const int h = s_cnt;
+                const int h = s_cnt[cs];
+                ++ci;
                 if (nco + h > kCoCap) break;  // uniform; this stride opens the next round
                 wb = __shfl_sync(kFull, wb, 0);
                 if (hit) co[nco + wb + __popc(bm & lanemask_lt())] = (uint16_t)l;

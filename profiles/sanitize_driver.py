@@ -47,6 +47,15 @@ def main():
         step.run_epoch(planner, max_steps=6)          # native epoch loop
         planner.close()
     os.environ["WJ_ENC_TC"] = "0"
+    # the shared-first-anchor scorer, dense enough for several co-reached rounds
+    g2 = wj.Graph.from_edges(rng.integers(0, 300, size=(6000, 2)), 300)
+    s2 = wj.preprocess(g2, 64, 4, 8)
+    p2 = wj.init_params(2, 4, dropout=0.1, seed=4)
+    qs = np.concatenate([np.stack([np.full(40, u), rng.integers(0, 300, 40)], 1)
+                         for u in rng.choice(300, 3, replace=False)]).astype(np.int64)
+    os.environ["WJ_SCORE_SHARED"] = "1"
+    wj.score_array(s2, p2, qs)
+    del os.environ["WJ_SCORE_SHARED"]
     et = wj.edge_types_from_node_types(g, (np.arange(n) % 2), 2)
     wj.preprocess_typed(g, et, [1, 2], 10, 3, 4)      # typed sampler
     torch.cuda.synchronize()
