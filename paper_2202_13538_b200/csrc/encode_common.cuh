@@ -41,6 +41,7 @@ struct EncMmaArgs {
     float *s_out;   // [B, AW, 64] or null
     float *msum;    // [B, 64] or null
     int32_t *qsched;  // [2] zeroed query-grab / done counters (dynamic scheduling) or null: static striding
+    int qsched_reset_by_tail;  // 1: the step's tail kernel zeroes qsched after its wait (no end-of-CTA reset)
     // dynamic scheduling over groups of identical queries (null: one query
     // per unit): [G | start[0..G] | order[0..B)] -- unit u = the queries
     // order[start[u] .. start[u+1]), all with the same anchor tuple, so the

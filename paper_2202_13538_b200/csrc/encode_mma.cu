@@ -435,7 +435,10 @@ __global__ void __launch_bounds__(kMW * 32, MINB) join_encode_mma_kernel(EncMmaA
         }  // members
         u = nb;
     }
-    if (dyn && threadIdx.x == 0) {
+    // the step executor's tail zeroes the counters once this grid completed;
+    // standalone launches: the last CTA to finish does (a fence + an L2 round
+    // trip on every CTA's exit, which delays the dependent tail)
+    if (dyn && !g.qsched_reset_by_tail && threadIdx.x == 0) {
         __threadfence();
         if (atomicAdd(g.qsched + 1, 1) == (int)gridDim.x - 1) {  // every CTA is done grabbing
             atomicExch(g.qsched, 0);
@@ -1111,8 +1114,14 @@ extern "C" int wj_stepper_destroy(wj_stepper *st) {
     return WJ_OK;
 }
 
-extern "C" int wj_stepper_encode(wj_stepper *st, const int64_t *queries, int64_t n_batch, const int32_t *groups,
-                                 int64_t n_groups, wj_stream_t stream) {
+namespace wj {
+int encoder_tail(const float *, const float *, const float *, const float *, int64_t, int32_t, int32_t, const float *,
+                 const int32_t *, float, float *, float *, int32_t, int32_t, float, int64_t *, cudaStream_t,
+                 int32_t *sched_reset);
+}
+
+static int stepper_encode(wj_stepper *st, const int64_t *queries, int64_t n_batch, const int32_t *groups,
+                          int64_t n_groups, wj_stream_t stream, bool tail_follows) {
     using namespace wj;
     if (!st || !queries || n_batch < 1 || (groups && (n_groups < 1 || n_groups > n_batch))) {
         set_error("wj_stepper_encode: bad arguments");
@@ -1127,6 +1136,7 @@ extern "C" int wj_stepper_encode(wj_stepper *st, const int64_t *queries, int64_t
     g.n_batch = n_batch;
     g.groups = groups;
     g.n_units = groups ? n_groups : n_batch;
+    g.qsched_reset_by_tail = tail_follows ? 1 : 0;
     const int64_t blocks = g.n_units < st->plan.slots ? g.n_units : st->plan.slots;
     cudaError_t e = launch_pdl(st->plan.k, dim3((unsigned)blocks), dim3(st->plan.threads), st->plan.smem,
                                (cudaStream_t)stream, g);
@@ -1135,6 +1145,11 @@ extern "C" int wj_stepper_encode(wj_stepper *st, const int64_t *queries, int64_t
         return WJ_ERR_CUDA;
     }
     return check_launch("wj_stepper_encode");
+}
+
+extern "C" int wj_stepper_encode(wj_stepper *st, const int64_t *queries, int64_t n_batch, const int32_t *groups,
+                                 int64_t n_groups, wj_stream_t stream) {
+    return stepper_encode(st, queries, n_batch, groups, n_groups, stream, false);
 }
 
 extern "C" int wj_stepper_run(wj_stepper *st, const int64_t *queries, const float *labels, int64_t n_batch,
@@ -1148,13 +1163,14 @@ extern "C" int wj_stepper_run(wj_stepper *st, const int64_t *queries, const floa
         set_error("wj_stepper_run: query groups need the dynamic scheduler (sched)");
         return WJ_ERR_ARG;
     }
-    const int rc0 = wj_stepper_encode(st, queries, n_batch, groups, n_groups, stream);
+    const int rc0 = stepper_encode(st, queries, n_batch, groups, n_groups, stream, st->args.qsched != nullptr);
     if (rc0 != WJ_OK) return rc0;
     EncMmaArgs g = st->args;
     int64_t rows = (n_batch + 15) / 16;
     if (rows > st->tail_rows_max) rows = st->tail_rows_max;
-    int rc = wj_encoder_tail(g.pooled, g.s_out, g.msum, labels, n_batch, st->aw, 64, st->params, st->offsets9,
-                             st->scale, nullptr, st->partial, (int32_t)rows, nullptr, st->step, stream);
+    int rc = encoder_tail(g.pooled, g.s_out, g.msum, labels, n_batch, st->aw, 64, st->params, st->offsets9,
+                          st->scale, nullptr, st->partial, (int32_t)rows, 0, 0.f, st->step, (cudaStream_t)stream,
+                          g.qsched);
     if (rc != WJ_OK) return rc;
     return wj_adam(st->params, st->m, st->v, st->partial, (int32_t)rows, st->n_params, st->lr, st->beta1, st->beta2,
                    st->eps, st->step, nullptr, loss_out, stream);
@@ -1171,21 +1187,18 @@ extern "C" int wj_stepper_grads(wj_stepper *st, const int64_t *queries, const fl
         set_error("wj_stepper_grads: bad arguments");
         return WJ_ERR_ARG;
     }
-    const int rc0 = wj_stepper_encode(st, queries, n_batch, groups, n_groups, stream);
+    const int rc0 = stepper_encode(st, queries, n_batch, groups, n_groups, stream, st->args.qsched != nullptr);
     if (rc0 != WJ_OK) return rc0;
     EncMmaArgs g = st->args;
     int64_t rows = (n_batch + 15) / 16;
     if (rows > st->tail_rows_max) rows = st->tail_rows_max;
-    int rc = wj_encoder_tail(g.pooled, g.s_out, g.msum, labels, n_batch, st->aw, 64, st->params, st->offsets9,
-                             st->scale, nullptr, st->partial, (int32_t)rows, nullptr, st->step, stream);
+    int rc = encoder_tail(g.pooled, g.s_out, g.msum, labels, n_batch, st->aw, 64, st->params, st->offsets9,
+                          st->scale, nullptr, st->partial, (int32_t)rows, 0, 0.f, st->step, (cudaStream_t)stream,
+                          g.qsched);
     if (rc != WJ_OK) return rc;
     return wj_sum_partials(st->partial, (int32_t)rows, st->n_params + 1, grad_out, stream);
 }
 
-namespace wj {
-int encoder_tail(const float *, const float *, const float *, const float *, int64_t, int32_t, int32_t, const float *,
-                 const int32_t *, float, float *, float *, int32_t, int32_t, float, int64_t *, cudaStream_t);
-}
 
 // Batch-sharded data parallel: this rank's slice of one global
 // batch -- queries [b_offset, b_offset + n_batch) of b_global, whose tail rows
@@ -1208,13 +1221,13 @@ extern "C" int wj_stepper_grads_shard(wj_stepper *st, const int64_t *queries, co
         return WJ_ERR_ARG;
     }
     st->args.b_offset = b_offset;
-    const int rc0 = wj_stepper_encode(st, queries, n_batch, groups, n_groups, stream);
+    const int rc0 = stepper_encode(st, queries, n_batch, groups, n_groups, stream, st->args.qsched != nullptr);
     st->args.b_offset = 0;
     if (rc0 != WJ_OK) return rc0;
     EncMmaArgs g = st->args;
     return encoder_tail(g.pooled, g.s_out, g.msum, labels, n_batch, st->aw, 64, st->params, st->offsets9, st->scale,
                         nullptr, partial_out, rows, per_cta, 1.f / (float)b_global, st->step,
-                        (cudaStream_t)stream);
+                        (cudaStream_t)stream, g.qsched);
 }
 
 // Adam on the gathered partial rows of a batch-sharded step (fixed order)

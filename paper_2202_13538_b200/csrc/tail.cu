@@ -42,6 +42,7 @@ struct TailArgs {
     float *partial;       // [grid, total + 1] (last column: loss partial)
     float *work;          // [B, kVecStride] per-query vectors (training)
     int per_cta;          // queries per gradient CTA
+    int32_t *sched_reset; // [2] join+encode queue counters, zeroed after the wait (nullable)
 };
 
 // Sum the per-CTA partial gradients in a fixed order and apply Adam
@@ -321,6 +322,9 @@ __global__ void __launch_bounds__(kTW * 32) tail_tc_kernel(TailArgs g) {
     }
     pdl_wait();     // pooled / S / msum of the join+encode kernel
     pdl_trigger();  // the Adam kernel may get scheduled
+    // the join+encode grid has completed: zero its queue counters for the
+    // next step (its CTAs skip the end-of-CTA reset under the step executor)
+    if (g.sched_reset && blockIdx.x == 0 && tid < 2) g.sched_reset[tid] = 0;
     constexpr int NW1 = ((AW + 1) * 64 + NT - 1) / NT;
     // dW2 / dU1 tiles of this warp: m-tile (warp & 3), n-tiles 4 (warp >> 2) .. +3
     const int fm = warp & 3, fn = (warp >> 2) * 4;
@@ -373,8 +377,11 @@ __global__ void __launch_bounds__(kTW * 32) tail_tc_kernel(TailArgs g) {
             Z2[(gq + 8) * kTP + c + 1] = fmaf(az[3], g.scale, C1P[c + 1]);
             __syncthreads();
         }
-        // logits, BCE and dz2 (warp w: queries w, w + 8)
-        for (int q = warp; q < kTQ; q += kTW) {
+        // logits, BCE and dz2 (warp w: queries w, w + 8; unrolled, so the two
+        // shuffle / exp chains interleave; accumulation order unchanged)
+#pragma unroll
+        for (int qi = 0; qi < kTQ / kTW; ++qi) {
+            const int q = warp + qi * kTW;
             const float za = Z2[q * kTP + lane], zb = Z2[q * kTP + lane + 32];
             float part = fmaxf(za, 0.f) * u2a + fmaxf(zb, 0.f) * u2b;
 #pragma unroll
@@ -442,7 +449,9 @@ __global__ void __launch_bounds__(kTW * 32) tail_tc_kernel(TailArgs g) {
             const float *V = tid < 64 ? DHQ : DZ2;
             for (int q = 0; q < nq; ++q) vacc += V[q * kTP + (tid & 63)];
         }
-        __syncthreads();
+        // the next chunk overwrites the chunk buffers (the epilogue below only
+        // uses registers and vsm: no barrier after the last chunk)
+        if (q0 + kTQ < q_hi) __syncthreads();
     }
     if (g.step_inc && blockIdx.x == 0 && tid == 0) *g.step_inc += 1;
     if (!train) return;
@@ -518,7 +527,7 @@ namespace wj {
 int encoder_tail(const float *pooled, const float *s, const float *msum, const float *labels, int64_t n_batch,
                  int32_t aw, int32_t hidden, const float *params, const int32_t *offsets9, float scale,
                  float *logits_out, float *partial, int32_t partial_rows, int32_t per_cta, float inv_b,
-                 int64_t *step_inc, cudaStream_t stream) {
+                 int64_t *step_inc, cudaStream_t stream, int32_t *sched_reset) {
     if (hidden != kH) {
         set_error("encoder tail kernel supports hidden=64 (got %d)", hidden);
         return WJ_ERR_UNSUPPORTED;
@@ -556,6 +565,7 @@ int encoder_tail(const float *pooled, const float *s, const float *msum, const f
     g.partial = partial;
     g.work = nullptr;
     g.step_inc = step_inc;
+    g.sched_reset = sched_reset;
     const int64_t rows = labels ? partial_rows : (n_batch + kTQ - 1) / kTQ;
     g.per_cta = per_cta > 0 ? per_cta : (int)((n_batch + rows - 1) / rows);
     // the smem attribute is per (device, kernel): set once (a repeat is harmless)
@@ -588,7 +598,7 @@ extern "C" int wj_encoder_tail(const float *pooled, const float *s, const float 
                                int64_t *step_inc, wj_stream_t stream) {
     (void)work;  // not needed by the tensor-core tail (kept for ABI stability)
     return wj::encoder_tail(pooled, s, msum, labels, n_batch, aw, hidden, params, offsets9, scale, logits_out,
-                            partial, partial_rows, 0, 0.f, step_inc, (cudaStream_t)stream);
+                            partial, partial_rows, 0, 0.f, step_inc, (cudaStream_t)stream, nullptr);
 }
 
 extern "C" int wj_adam(float *params, float *m, float *v, const float *partial,
