@@ -223,25 +223,39 @@ __global__ void __launch_bounds__(kCountWarps * 32) rpe_count_hash_kernel(
         for (int i = lane * 4; i < T; i += 128) *reinterpret_cast<uint4 *>(tab + i) = make_uint4(~0u, ~0u, ~0u, ~0u);
         __syncwarp();
         const int32_t *src = walks + k * (int64_t)P;
+        // landings equal to the anchor (every walk's step 0, and returns) are
+        // not inserted -- one same-address CAS per such slot serialised the
+        // warp -- the anchor counts once (it is present: it is slot 0); the
+        // next round's keys are loaded before this round's probes
         int count = 0;
+        bool has_u = false;
+        int32_t xn = lane < P ? __ldg(src + lane) : 0;
+        const int32_t u = __shfl_sync(kFull, xn, 0);  // walk 0's step 0: the anchor (any value is exact)
         for (int base = 0; base < P; base += 32) {
             const int i = base + lane;
+            const int32_t xs = xn;
+            xn = i + 32 < P ? __ldg(src + i + 32) : 0;
             bool fresh = false;
             if (i < P) {
-                const uint32_t x = (uint32_t)__ldg(src + i);
-                uint32_t h = (x * 0x9E3779B1u) >> (32 - tbits);
-                while (true) {
-                    const uint32_t old = atomicCAS(tab + h, ~0u, x);
-                    if (old == ~0u) {
-                        fresh = true;
-                        break;
+                if (xs == u) {
+                    has_u = true;
+                } else {
+                    const uint32_t x = (uint32_t)xs;
+                    uint32_t h = (x * 0x9E3779B1u) >> (32 - tbits);
+                    while (true) {
+                        const uint32_t old = atomicCAS(tab + h, ~0u, x);
+                        if (old == ~0u) {
+                            fresh = true;
+                            break;
+                        }
+                        if (old == x) break;
+                        h = (h + 1) & (T - 1);
                     }
-                    if (old == x) break;
-                    h = (h + 1) & (T - 1);
                 }
             }
             count += __popc(__ballot_sync(kFull, fresh));
         }
+        count += __any_sync(kFull, has_u) ? 1 : 0;
         if (lane == 0) counts_out[k] = count;
         __syncwarp();
     }
