@@ -56,9 +56,15 @@ __global__ void __launch_bounds__(kInternThreads) intern_insert_kernel(
             uint32_t h = (uint32_t)(mix64(key) & (kSmemSlots - 1));
             bool done = false;
             for (int probes = 0; probes < 64; ++probes) {
-                const unsigned long long prev = atomicCAS(&skeys[h], kEmpty, key);
+                // a slot only ever goes empty -> key, so a plain read that sees
+                // the key needs no atomic (the hot vectors hit the same few
+                // slots from every lane: a CAS / min per entry serialised them);
+                // the scan order only needs an atomic when it would lower it
+                unsigned long long prev = *reinterpret_cast<volatile unsigned long long *>(&skeys[h]);
+                if (prev == kEmpty) prev = atomicCAS(&skeys[h], kEmpty, key);
                 if (prev == kEmpty || prev == key) {
-                    atomicMin(&sorder[h], (unsigned long long)ord);
+                    if ((unsigned long long)ord < *reinterpret_cast<volatile unsigned long long *>(&sorder[h]))
+                        atomicMin(&sorder[h], (unsigned long long)ord);
                     done = true;
                     break;
                 }
