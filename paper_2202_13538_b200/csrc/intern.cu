@@ -50,27 +50,40 @@ __global__ void __launch_bounds__(kInternThreads) intern_insert_kernel(
          k += (int64_t)gridDim.x * nwarps) {
         const int64_t lo = offsets[k], hi = offsets[k + 1];
         const uint64_t ahi = (uint64_t)(anchor_base + k) << 16;
-        for (int64_t e = lo + lane; e < hi; e += 32) {
-            const uint64_t key = ukey[e];
-            const uint64_t ord = ahi | ufirst[e];
-            uint32_t h = (uint32_t)(mix64(key) & (kSmemSlots - 1));
-            bool done = false;
-            for (int probes = 0; probes < 64; ++probes) {
-                // a slot only ever goes empty -> key, so a plain read that sees
-                // the key needs no atomic (the hot vectors hit the same few
-                // slots from every lane: a CAS / min per entry serialised them);
-                // the scan order only needs an atomic when it would lower it
-                unsigned long long prev = *reinterpret_cast<volatile unsigned long long *>(&skeys[h]);
-                if (prev == kEmpty) prev = atomicCAS(&skeys[h], kEmpty, key);
-                if (prev == kEmpty || prev == key) {
-                    if ((unsigned long long)ord < *reinterpret_cast<volatile unsigned long long *>(&sorder[h]))
-                        atomicMin(&sorder[h], (unsigned long long)ord);
-                    done = true;
-                    break;
-                }
-                h = (h + 1) & (kSmemSlots - 1);
+        // four entries per lane in flight (the loads, not the table, bound
+        // this pass), then inserted in entry order
+        for (int64_t e0 = lo + lane; e0 < hi; e0 += 4 * 32) {
+            uint64_t kv[4];
+            uint16_t fv[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int64_t e = e0 + 32 * j;
+                kv[j] = e < hi ? __ldg(ukey + e) : kEmpty;
+                fv[j] = e < hi ? __ldg(ufirst + e) : (uint16_t)0;
             }
-            if (!done && !global_insert(gkeys, gorder, gmask, key, ord)) *overflow = 1;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint64_t key = kv[j];
+                if (key == kEmpty) continue;
+                const uint64_t ord = ahi | fv[j];
+                uint32_t h = (uint32_t)(mix64(key) & (kSmemSlots - 1));
+                bool done = false;
+                for (int probes = 0; probes < 64; ++probes) {
+                    // a slot only ever goes empty -> key, so a plain read that
+                    // sees the key needs no atomic; the scan order only needs
+                    // an atomic when it would lower it
+                    unsigned long long prev = *reinterpret_cast<volatile unsigned long long *>(&skeys[h]);
+                    if (prev == kEmpty) prev = atomicCAS(&skeys[h], kEmpty, key);
+                    if (prev == kEmpty || prev == key) {
+                        if ((unsigned long long)ord < *reinterpret_cast<volatile unsigned long long *>(&sorder[h]))
+                            atomicMin(&sorder[h], (unsigned long long)ord);
+                        done = true;
+                        break;
+                    }
+                    h = (h + 1) & (kSmemSlots - 1);
+                }
+                if (!done && !global_insert(gkeys, gorder, gmask, key, ord)) *overflow = 1;
+            }
         }
     }
     __syncthreads();
@@ -84,21 +97,33 @@ __global__ void intern_assign_kernel(const uint64_t *__restrict__ ukey, int64_t 
                                      const uint64_t *__restrict__ gkeys,
                                      const int32_t *__restrict__ gids, uint64_t gmask,
                                      int32_t *__restrict__ uid) {
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const uint64_t key = ukey[e];
-        uint64_t h = mix64(key) & gmask;
-        int32_t id = 0;
-        for (uint64_t probes = 0; probes <= gmask; ++probes) {
-            const uint64_t k = __ldg(gkeys + h);
-            if (k == key) {
-                id = __ldg(gids + h);
-                break;
-            }
-            if (k == kEmpty) break;
-            h = (h + 1) & gmask;
+    // four entries per thread in flight (grid-strided, coalesced)
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < n; e0 += 4 * stride) {
+        uint64_t kv[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t e = e0 + j * stride;
+            kv[j] = e < n ? __ldg(ukey + e) : kEmpty;
         }
-        uid[e] = id;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t e = e0 + j * stride;
+            if (e >= n) break;
+            const uint64_t key = kv[j];
+            uint64_t h = mix64(key) & gmask;
+            int32_t id = 0;
+            for (uint64_t probes = 0; probes <= gmask; ++probes) {
+                const uint64_t k = __ldg(gkeys + h);
+                if (k == key) {
+                    id = __ldg(gids + h);
+                    break;
+                }
+                if (k == kEmpty) break;
+                h = (h + 1) & gmask;
+            }
+            uid[e] = id;
+        }
     }
 }
 

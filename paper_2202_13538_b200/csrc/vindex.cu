@@ -37,10 +37,17 @@ __global__ void vindex_count_kernel(const int64_t *__restrict__ off, const int32
     if (u >= n) return;
     const int64_t lo = off[u], hi = off[u + 1];
     int c2 = 0, c1 = 0;
-    for (int64_t e = lo + lane; e < hi; e += 32) {
-        const int r = row_sum(__ldg(tk + __ldg(uid + e)), cb, W);
-        c2 += r >> 1;
-        c1 += r & 1;
+    for (int64_t e0 = lo + lane; e0 < hi; e0 += 4 * 32) {  // four ids per lane in flight
+        int32_t id[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) id[j] = e0 + 32 * j < hi ? __ldg(uid + e0 + 32 * j) : -1;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (id[j] < 0) continue;
+            const int r = row_sum(__ldg(tk + id[j]), cb, W);
+            c2 += r >> 1;
+            c1 += r & 1;
+        }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
