@@ -201,7 +201,10 @@ def upload(arr: np.ndarray, device) -> torch.Tensor:
         # the new block may have been freed by work still queued on this
         # stream; wj_upload writes from its own streams
         torch.cuda.current_stream(device).synchronize()
-        threads = max(1, min(8, (os.cpu_count() or 2) // 2))
+        # WJ_UPLOAD_THREADS: override (the batch planner's build runs on the
+        # other host cores at the same time in train() / the e2e bench)
+        env = os.environ.get("WJ_UPLOAD_THREADS")
+        threads = int(env) if env else max(1, min(8, (os.cpu_count() or 2) // 2))
         _lib.call("wj_upload", out.data_ptr(), arr.ctypes.data, arr.nbytes, threads)
     return out
 

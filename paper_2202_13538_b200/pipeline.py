@@ -261,6 +261,7 @@ class BatchPlanner:
                  None if pl is None else pl.ctypes.data, 0 if pl is None else pl.shape[0], ctypes.byref(self._h))
         self._words = _rng_words(rng)
         self._builder, self._build_err = None, None
+        self.depth = int(depth)
         if background:
             # the build (query index + positive-tuple set, ~0.15 s at C3) runs on
             # a host thread -- ctypes releases the GIL -- e.g. while the device
@@ -270,6 +271,9 @@ class BatchPlanner:
             def build():
                 try:
                     _lib.call("wj_planner_create", *cargs)
+                    # the pinned ring too (a cudaHostAlloc per buffer: ~7 ms
+                    # that would otherwise sit before the preprocess)
+                    self._alloc_ring(pinned)
                 except BaseException as e:  # re-raised by wait()
                     self._build_err = e
 
@@ -278,18 +282,22 @@ class BatchPlanner:
         else:
             _lib.call("wj_planner_create", *cargs)
             _lib.call("wj_planner_set_rng", self._h, self._words.ctypes.data)
-        mk = (lambda t: t.pin_memory()) if pinned and torch.cuda.is_available() else (lambda t: t)
-        self.depth = int(depth)
-        self._q = mk(torch.empty((self.depth, self.cap, self.arity), dtype=torch.int64))
-        self._y = mk(torch.empty((self.depth, self.cap), dtype=torch.float32))
-        # per slot: units of identical queries [G | start[0..G] | order | tuple] (wj_group_queries)
-        self._g = mk(torch.empty((self.depth, (2 + self.arity) * self.cap + 2), dtype=torch.int32))
+            self._alloc_ring(pinned)
         self.groups_view = None
         self._ev = [None] * self.depth
         self._i = 0
         self._cur = 0
         self._running = False
         self._out = (ctypes.c_int64 * 3)()
+
+    def _alloc_ring(self, pinned: bool) -> None:
+        """The planner's ring of batch slots (pinned: the H2D copies and the
+        native epoch loop read them in place)."""
+        mk = (lambda t: t.pin_memory()) if pinned and torch.cuda.is_available() else (lambda t: t)
+        self._q = mk(torch.empty((self.depth, self.cap, self.arity), dtype=torch.int64))
+        self._y = mk(torch.empty((self.depth, self.cap), dtype=torch.float32))
+        # per slot: units of identical queries [G | start[0..G] | order | tuple] (wj_group_queries)
+        self._g = mk(torch.empty((self.depth, (2 + self.arity) * self.cap + 2), dtype=torch.int32))
 
     def wait(self) -> None:
         """Block until a background build has finished (no-op otherwise)."""
