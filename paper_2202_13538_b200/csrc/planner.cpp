@@ -250,12 +250,17 @@ struct wj_planner {
     std::vector<int64_t> seed_list, queue, batch, draws;
     std::vector<uint64_t> hashes, keys1;
     std::vector<Key2> keys2;
-    // epoch producer thread (wj_planner_start_epoch): fills a caller-owned
-    // ring of batch slots in order; slot_ready[s] is 0 (free) / 1 (ready)
+    // epoch producer (wj_planner_start_epoch): two threads fill a caller-owned
+    // ring of batch slots in order -- the planner thread plans a batch into a
+    // slot (slot_ready 0 -> 1, its seed set copied to slot_seeds), the
+    // grouping thread groups it (1 -> 2: ready), so grouping batch b overlaps
+    // planning batch b + 1; the consumer acquires a ready slot and releases
+    // it (-> 0)
     struct Slot {
         int64_t n_queries, n_pos;  // n_queries -1: end of epoch; -2: error
     };
-    std::thread worker;
+    std::thread worker, grouper;
+    std::vector<std::vector<int64_t>> slot_seeds;
     std::atomic<int> stop{0};
     bool running = false;
     int64_t *ring_q = nullptr;
@@ -271,6 +276,7 @@ struct wj_planner {
     ~wj_planner() {
         stop.store(1);
         if (worker.joinable()) worker.join();
+        if (grouper.joinable()) grouper.join();
     }
 };
 
@@ -718,8 +724,8 @@ int plan_one(wj_planner *p, int64_t *queries_out, float *labels_out, int64_t cap
 // thread.  Every node of the batch is in its seed set, so for pairs over a
 // small seed set the tuple id comes from a dense (local a, local b) table
 // instead of hashing the tuples; otherwise wj_group_queries.
-void group_planned(wj_planner *p, const int64_t *q, int64_t n, int32_t *out) {
-    const int64_t ns = (int64_t)p->seed_list.size();
+void group_planned(wj_planner *p, const std::vector<int64_t> &seed_list, const int64_t *q, int64_t n, int32_t *out) {
+    const int64_t ns = (int64_t)seed_list.size();
     if (p->arity != 2 || ns > 128 || !p->pool.empty()) {
         wj_group_queries(q, n, p->arity, p->group_max, out, nullptr);
         return;
@@ -731,7 +737,7 @@ void group_planned(wj_planner *p, const int64_t *q, int64_t n, int32_t *out) {
     p->sset.assign((size_t)1 << sbits, -1);
     p->sidx.assign((size_t)1 << sbits, 0);
     for (int64_t i = 0; i < ns; ++i) {
-        const int64_t a = p->seed_list[i];
+        const int64_t a = seed_list[i];
         uint64_t h = hash_of((uint64_t)a) >> (64 - sbits);
         while (p->sset[h] >= 0) h = (h + 1) & smask;
         p->sset[h] = a;
@@ -787,13 +793,28 @@ void epoch_worker(wj_planner *p) {
             m.n_queries = rc != WJ_OK ? -2 : (npos == 0 ? -1 : nq);
             m.n_pos = npos;
             consumed += npos;
-            if (rc == WJ_OK && nq > 0 && p->ring_g)
-                group_planned(p, p->ring_q + (int64_t)s * p->ring_cap * p->arity, nq,
-                              p->ring_g + (int64_t)s * ((2 + p->arity) * p->ring_cap + 2));
+            if (m.n_queries > 0 && p->ring_g) p->slot_seeds[s] = p->seed_list;  // the grouper's copy
         }
         const bool last = m.n_queries < 0;
         p->slot_ready[s].store(1, std::memory_order_release);
         if (last) return;
+    }
+}
+
+// the grouping stage of the epoch producer (see wj_planner)
+void group_worker(wj_planner *p) {
+    for (int64_t b = 0;; ++b) {
+        const int32_t s = (int32_t)(b % p->n_slots);
+        while (p->slot_ready[s].load(std::memory_order_acquire) != 1) {
+            if (p->stop.load(std::memory_order_relaxed)) return;
+            std::this_thread::yield();
+        }
+        const auto m = p->slot_meta[s];
+        if (m.n_queries > 0 && p->ring_g)
+            group_planned(p, p->slot_seeds[s], p->ring_q + (int64_t)s * p->ring_cap * p->arity, m.n_queries,
+                          p->ring_g + (int64_t)s * ((2 + p->arity) * p->ring_cap + 2));
+        p->slot_ready[s].store(2, std::memory_order_release);
+        if (m.n_queries < 0) return;
     }
 }
 
@@ -834,10 +855,12 @@ extern "C" int wj_planner_start_epoch(wj_planner *p, int64_t *ring_queries, floa
     p->slot_ready.reset(new std::atomic<int>[n_slots]);
     for (int32_t i = 0; i < n_slots; ++i) p->slot_ready[i].store(0);
     p->slot_meta.assign(n_slots, {0, 0});
+    p->slot_seeds.assign(n_slots, {});
     p->worker_err[0] = 0;
     p->stop.store(0);
     p->running = true;
     p->worker = std::thread(epoch_worker, p);
+    p->grouper = std::thread(group_worker, p);
     return WJ_OK;
 }
 
@@ -847,14 +870,15 @@ extern "C" int wj_planner_acquire(wj_planner *p, int32_t *slot_out, int64_t *n_q
         return WJ_ERR_ARG;
     }
     const int32_t s = (int32_t)(p->consumed_batches % p->n_slots);
-    while (p->slot_ready[s].load(std::memory_order_acquire) == 0) {
+    while (p->slot_ready[s].load(std::memory_order_acquire) != 2) {
 #if defined(__x86_64__)
         __builtin_ia32_pause();
 #endif
     }
     const auto m = p->slot_meta[s];
-    if (m.n_queries < 0) {  // end of epoch or error: the producer has returned
+    if (m.n_queries < 0) {  // end of epoch or error: both producer threads have returned
         p->worker.join();
+        p->grouper.join();
         p->running = false;
         *slot_out = -1;
         *n_queries_out = 0;
@@ -885,6 +909,7 @@ extern "C" int wj_planner_stop(wj_planner *p) {
     if (!p) return WJ_OK;
     p->stop.store(1);
     if (p->worker.joinable()) p->worker.join();
+    if (p->grouper.joinable()) p->grouper.join();
     p->running = false;
     return WJ_OK;
 }

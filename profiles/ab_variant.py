@@ -19,6 +19,7 @@ def main():
     out = os.path.join(ROOT, "ab")
     os.makedirs(out, exist_ok=True)
     flags = [f for f in B.FLAGS if f not in ("-shared", "-cudart", "static")]
+    flags += os.environ.get("ABV_FLAGS", "").split()  # e.g. ABV_FLAGS=-maxrregcount=152
     objs = []
     for src in B.SOURCES:
         if src in repl:
