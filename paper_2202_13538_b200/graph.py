@@ -201,10 +201,13 @@ def upload(arr: np.ndarray, device) -> torch.Tensor:
         # the new block may have been freed by work still queued on this
         # stream; wj_upload writes from its own streams
         torch.cuda.current_stream(device).synchronize()
-        # WJ_UPLOAD_THREADS: override (the batch planner's build runs on the
-        # other host cores at the same time in train() / the e2e bench)
+        # 8 staging threads, or 2 while a background batch-planner build runs
+        # (it is host-core / DRAM bound: at C3, t_pre 145-152 ms with 8 upload
+        # threads vs 119-126 ms with 2); WJ_UPLOAD_THREADS overrides
+        from .pipeline import planner_builds_in_flight
+
         env = os.environ.get("WJ_UPLOAD_THREADS")
-        threads = int(env) if env else max(1, min(8, (os.cpu_count() or 2) // 2))
+        threads = int(env) if env else (2 if planner_builds_in_flight() else max(1, min(8, (os.cpu_count() or 2) // 2)))
         _lib.call("wj_upload", out.data_ptr(), arr.ctypes.data, arr.nbytes, threads)
     return out
 

@@ -228,6 +228,22 @@ def _rng_words(rng: np.random.Generator) -> np.ndarray:
                     dtype=np.uint64)
 
 
+# background planner builds in flight: the build is DRAM / core bound on the
+# host, so a concurrent host -> device upload (graph.upload) uses fewer threads
+_builds_lock = threading.Lock()
+_builds_in_flight = 0
+
+
+def planner_builds_in_flight() -> int:
+    return _builds_in_flight
+
+
+def _build_count(delta: int) -> None:
+    global _builds_in_flight
+    with _builds_lock:
+        _builds_in_flight += delta
+
+
 class BatchPlanner:
     """Training batches from the native planner (csrc/planner.cpp,
     ``wj_planner_*``): the reference's ``sample_minibatch`` +
@@ -276,8 +292,11 @@ class BatchPlanner:
                     self._alloc_ring(pinned)
                 except BaseException as e:  # re-raised by wait()
                     self._build_err = e
+                finally:
+                    _build_count(-1)
 
             self._builder = threading.Thread(target=build, name="wj-planner-build", daemon=True)
+            _build_count(1)
             self._builder.start()
         else:
             _lib.call("wj_planner_create", *cargs)
